@@ -1,0 +1,197 @@
+/*
+ * socfield_cuda.h — the C ABI of the B200 (sm_100a) engine for the per-tick hot path of the
+ * discrete social-field pedestrian model.
+ *
+ * This is the drop-in boundary.  The reference has no FFI: its boundary is the C++ class
+ * socfield::Engine acting on the value type socfield::SimState
+ * (reference proj/include/socfield/engine.hpp:91-98,142-230).  The host mirror in
+ * include/socfield/ keeps that class signature for signature and forwards every device
+ * operation through the entry points below — plain pointers and sizes, no C++ or torch
+ * types, no exceptions across the line.  Each entry point names the reference interface it
+ * replaces.
+ *
+ * Threading: an sfc_engine is not thread-safe; every call is synchronous for the caller
+ * (the reference's Engine::tick is synchronous too, engine.hpp:150-158).
+ */
+#ifndef SOCFIELD_CUDA_H
+#define SOCFIELD_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFC_ABI_VERSION 1
+#define SFC_KINDS 3 /* dir-attractive, dir-repulsive, recurrent-repulsive (engine.hpp:19) */
+#define SFC_SECTS 8
+
+/* Status codes.  The host mirror rethrows them as the reference's exception types
+ * (errors.hpp): INTEGRITY -> IntegrityError(tick, phase), CONFIG -> ConfigError,
+ * everything else -> std::runtime_error. */
+enum {
+    SFC_OK = 0,
+    SFC_E_INTEGRITY = -1,
+    SFC_E_CONFIG = -2,
+    SFC_E_CUDA = -3,
+    SFC_E_NOMEM = -4,
+    SFC_E_STATE = -5, /* call sequence error, e.g. run before upload */
+    SFC_E_NO_DEVICE = -6
+};
+
+typedef struct sfc_engine sfc_engine;
+
+/* GridGeometry (grid.hpp:26-45) + EngineConfig (engine.hpp:108-121). */
+typedef struct sfc_config {
+    int32_t width, height;
+    int32_t closed;                /* BoundaryMode::Closed */
+    int32_t chunk_k;               /* K of the multi-step sum: 2, 4, 8 or 16 */
+    double weight_static, weight_dir_attractive, weight_dir_repulsive, weight_recurrent;
+    double goal_bias;
+    int32_t regulation;            /* 0 identity, 1 linear */
+    int32_t density_radius;
+    int64_t rebuild_interval;      /* 0 = never */
+    double rebuild_tolerance;
+    int32_t fault_invert_vote_tiebreak; /* test hook, engine.hpp:120 */
+    int32_t device;                /* CUDA device ordinal */
+    /* Row slab owned by this engine (multi-GPU): rows [slab_row0, slab_row0 + slab_rows).
+     * slab_rows = 0 means the whole grid. */
+    int32_t slab_row0, slab_rows;
+    int32_t reserved;
+} sfc_config;
+
+/* Merged contributor table of one dynamic kind, replacing Engine::build_gather_tables
+ * (engine.cpp:201-221).  Indexed by centre offset (dx, dy) = mover centre - target su:
+ * entry (dy + height/2) * width + (dx + width/2).
+ *   magnitude  strength the field incurs at the target (double, WritePlan::Entry::magnitude)
+ *   info       bits 0-2  sect of the (target, sect) address the offset feeds
+ *              bits 3-10 orientation mask (all ones for the non-directional kind; 0 = the
+ *                        offset is outside the support)
+ *              bits 11-31 j, the offset's rank in the (kind, sect) contributor list, ordered
+ *                        lexicographically by (dx, dy) — fixes the StepCache slot
+ *                        (accumulator.hpp:36-40)
+ * The host computes these with the same libm calls as the reference (fields.cpp:74-121). */
+typedef struct sfc_kind_table {
+    int32_t width, height;
+    const double* magnitude;
+    const uint32_t* info;
+} sfc_kind_table;
+
+typedef struct sfc_tables {
+    sfc_kind_table kind[SFC_KINDS];
+} sfc_tables;
+
+/* Host view of a SimState (engine.hpp:91-98): raw pointers into OccupancyGrid::raw(),
+ * StrengthImage::raw() and per-pedestrian attribute arrays gathered from
+ * std::vector<Pedestrian>.  Arrays marked [out] are written by sfc_download. */
+typedef struct sfc_state_view {
+    int64_t tick;                 /* [in/out] SimState::tick */
+    int64_t n_peds;
+    int32_t* occupancy;           /* [in/out] [H*W], -1 empty */
+    float* static_image;          /* [in]     [H*W*8] (may be NULL on download) */
+    float* dyn_images[SFC_KINDS]; /* [in/out] [H*W*8] each */
+    int32_t* center_xy;           /* [in/out] [P*2] */
+    const int32_t* walk_period;   /* [in] [P] */
+    const int32_t* walk_phase;    /* [in] [P] */
+    const int32_t* goal_sect;     /* [in] [P] */
+    const int32_t* orient_attractive; /* [in] [P] FieldSpec::orientation of the dir-attractive field */
+    const int32_t* orient_repulsive;  /* [in] [P] ... of the dir-repulsive field */
+    const int32_t* foot_w;        /* [in] [P] odd */
+    const int32_t* foot_h;        /* [in] [P] odd */
+} sfc_state_view;
+
+/* TickMetrics (engine.hpp:123-128); phase_us from CUDA events when requested. */
+typedef struct sfc_tick_metrics {
+    int64_t tick;
+    int64_t moved;
+    int64_t phase_us[5];
+    int64_t wall_us;
+} sfc_tick_metrics;
+
+/* Host mirrors of the per-tick temporaries the reference exposes through
+ * Engine::enrollment(), vote_winners(), movement_log(), decision_direction()
+ * (engine.hpp:172-177).  Any pointer may be NULL. */
+typedef struct sfc_temporaries {
+    int32_t* decisions;      /* [P] */
+    double* decision_scores; /* [P] */
+    int32_t* enroll_ids;     /* [C*8] */
+    double* enroll_scores;   /* [C*8] */
+    int32_t* winners;        /* [C] */
+    int32_t* moved_from;     /* [C] */
+    int32_t* moved_to;       /* [C] */
+    uint8_t* from_mask;      /* [3*C] */
+    uint8_t* to_mask;        /* [3*C] */
+} sfc_temporaries;
+
+/* A static field anchored at a su (fields.hpp:151-154 AnchoredField).  `table` is built by
+ * the host exactly like a dynamic kind's (info mask is 0xFF inside the support); anchors
+ * that share a FieldSpec share a table. */
+typedef struct sfc_anchor {
+    int32_t x, y;
+    int32_t table;       /* index into the tables array passed alongside */
+    int32_t orientation; /* facing sect of a directional field, -1 for non-directional kinds */
+} sfc_anchor;
+
+int sfc_abi_version(void);
+/* Number of visible CUDA devices (<= 0: none; the engine never falls back to the CPU). */
+int sfc_device_count(void);
+
+/* Engine::Engine (engine.cpp:170-199): validates the configuration, uploads the tables,
+ * allocates the SU field buffers and per-tick temporaries on the device. */
+int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out, char* err,
+               size_t errlen);
+void sfc_destroy(sfc_engine* e);
+
+/* Last error text and the (tick, phase, su) detail of an integrity violation. */
+const char* sfc_last_error(const sfc_engine* e);
+void sfc_error_detail(const sfc_engine* e, int64_t* tick, int32_t* phase, int32_t* su_x,
+                      int32_t* su_y, double* value);
+
+/* Host -> device copy of a whole SimState; device -> host copy of what a tick mutates
+ * (occupancy, dynamic images, centres, tick).  Engine::tick / Engine::run entry and exit. */
+int sfc_upload(sfc_engine* e, const sfc_state_view* view);
+int sfc_download(sfc_engine* e, sfc_state_view* view);
+
+/* Engine::run body (engine.cpp:556-563 minus verify_state): `ticks` iterations of
+ * Engine::tick (engine.cpp:478-536) including the periodic rebuild (engine.cpp:538-550), on
+ * the device-resident state.  metrics: NULL or [ticks].  with_phase_times != 0 brackets each
+ * phase with CUDA events (slower). */
+int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_phase_times);
+
+/* One phase of the current tick for the Engine::Inspector path (engine.hpp:150-155):
+ * phase 1..5 = k-1..k-5, 6 = end of tick (tick += 1, maybe_rebuild).  *moved is TickMetrics::moved
+ * (valid after phase 4). */
+int sfc_phase(sfc_engine* e, int phase, int64_t* moved);
+int sfc_download_temporaries(sfc_engine* e, sfc_temporaries* out);
+
+/* Engine::decide (engine.cpp:326-333) for one pedestrian of the uploaded state. */
+int sfc_decide(sfc_engine* e, int64_t ped, int32_t* direction, double* score);
+
+/* rasterize_dynamic / Engine::rebuild_images (engine.cpp:158-168,565-567) from the uploaded
+ * pedestrians: out[k] receives image k ([H*W*8] host floats).  The device images are untouched. */
+int sfc_rasterize_dynamic(sfc_engine* e, float* out[SFC_KINDS]);
+/* Same, but replaces the device-resident dynamic images (seed_population, scenario.cpp:427). */
+int sfc_reset_dynamic_images(sfc_engine* e);
+/* rasterize_static / rasterize_into (fields.cpp:152-168): adds the anchored fields, in list
+ * order, into the device static image — zeroed first, or initialised from `base` ([H*W*8] host
+ * floats) when that is not NULL — and copies the result to `out` ([H*W*8], may be NULL). */
+int sfc_rasterize_static(sfc_engine* e, int32_t n_tables, const sfc_kind_table* tables, int64_t n_anchors,
+                         const sfc_anchor* anchors, const float* base, float* out);
+
+/* Counters for bench.py: kernels launched by this engine since creation, bytes copied. */
+typedef struct sfc_counters {
+    int64_t kernel_launches;
+    int64_t graph_launches;
+    int64_t h2d_bytes, d2h_bytes;
+} sfc_counters;
+void sfc_get_counters(const sfc_engine* e, sfc_counters* out);
+
+/* CUDA-event time of the device work enqueued by the last sfc_run, in milliseconds, and the
+ * share spent in the k-5 write-back kernel when phase timing was requested. */
+double sfc_last_run_ms(const sfc_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

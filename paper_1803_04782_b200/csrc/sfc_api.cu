@@ -1,0 +1,706 @@
+// sfc_api.cu — the C ABI (include/socfield_cuda.h) over the sm_100a kernels.
+//
+// Owns the device-resident SimState, the per-tick temporaries and the CUDA stream / graph that
+// sequences k-2 -> k-3 -> k-4 -> k-5 (k-1 does not exist here: nothing needs a full-grid clear).
+// There is no CPU path: without a CUDA device sfc_create fails with SFC_E_NO_DEVICE.
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sfc_internal.cuh"
+
+using namespace sfc;
+
+struct sfc_engine {
+    sfc_config cfg{};
+    GridDev g{};
+    DecideParams dp{};
+    TablesDev tabs{};
+    std::vector<void*> table_allocs;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+
+    long long cells = 0; // resident su (slab rows + halos)
+    int* occ = nullptr;
+    float* stat = nullptr;
+    float* dyn = nullptr;
+    uint8_t* ev = nullptr;
+    PedArrays peds{};
+    long long ped_capacity = 0;
+    Ctl* ctl = nullptr;
+    unsigned long long* moved_counts = nullptr;
+    long long moved_capacity = 0;
+    DebugArrays dbg{};
+    float* stage = nullptr; // staging for layout conversion
+    long long stage_cells = 0;
+
+    cudaGraphExec_t graph = nullptr;
+    bool graph_valid = false;
+
+    bool uploaded = false;
+    long long tick = 0;
+    sfc_counters counters{};
+    double last_run_ms = 0.0;
+
+    std::string err;
+    long long err_tick = -1;
+    int err_phase = 0, err_x = 0, err_y = 0;
+    double err_value = 0.0;
+};
+
+namespace {
+
+constexpr long long kStageCells = 4ll << 20; // 4 Mi su per staging chunk (128 MiB of one image)
+
+int fail(sfc_engine* e, int code, const std::string& msg) {
+    e->err = msg;
+    return code;
+}
+
+int cuda_fail(sfc_engine* e, cudaError_t c, const char* what) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "CUDA error in %s: %s", what, cudaGetErrorString(c));
+    e->err = buf;
+    return c == cudaErrorMemoryAllocation ? SFC_E_NOMEM : SFC_E_CUDA;
+}
+
+#define SFC_CUDA(call)                                            \
+    do {                                                          \
+        cudaError_t c_ = (call);                                  \
+        if (c_ != cudaSuccess) return cuda_fail(e, c_, #call);    \
+    } while (0)
+
+template <class T>
+cudaError_t dev_alloc(T** p, long long n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (size_t)std::max<long long>(n, 1));
+}
+
+int upload_table(sfc_engine* e, const sfc_kind_table& src, KindTableDev* dst) {
+    if (src.width < 1 || src.height < 1 || src.width % 2 == 0 || src.height % 2 == 0)
+        return fail(e, SFC_E_CONFIG, "field_geometry: must be odd x odd");
+    if (src.width > 8000 || src.height > 8000) return fail(e, SFC_E_CONFIG, "field_geometry: support too large");
+    const size_t n = (size_t)src.width * src.height;
+    double* mag = nullptr;
+    uint32_t* info = nullptr;
+    SFC_CUDA(dev_alloc(&mag, (long long)n));
+    e->table_allocs.push_back(mag);
+    SFC_CUDA(dev_alloc(&info, (long long)n));
+    e->table_allocs.push_back(info);
+    SFC_CUDA(cudaMemcpy(mag, src.magnitude, sizeof(double) * n, cudaMemcpyHostToDevice));
+    SFC_CUDA(cudaMemcpy(info, src.info, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    dst->fw = src.width;
+    dst->fh = src.height;
+    dst->hw = (src.width - 1) / 2;
+    dst->hh = (src.height - 1) / 2;
+    dst->mag = mag;
+    dst->info = info;
+    return SFC_OK;
+}
+
+void free_peds(sfc_engine* e) {
+    cudaFree(e->peds.center);
+    cudaFree(e->peds.gate);
+    cudaFree(e->peds.attr);
+    cudaFree(e->peds.dir);
+    cudaFree(e->peds.score);
+    cudaFree(e->peds.won);
+    cudaFree(e->peds.moved_dir);
+    e->peds = PedArrays{};
+    e->ped_capacity = 0;
+}
+
+int ensure_peds(sfc_engine* e, long long n) {
+    if (n <= e->ped_capacity && e->peds.center) {
+        e->peds.n = n;
+        return SFC_OK;
+    }
+    free_peds(e);
+    e->graph_valid = false;
+    SFC_CUDA(dev_alloc(&e->peds.center, n));
+    SFC_CUDA(dev_alloc(&e->peds.gate, n));
+    SFC_CUDA(dev_alloc(&e->peds.attr, n));
+    SFC_CUDA(dev_alloc(&e->peds.dir, n));
+    SFC_CUDA(dev_alloc(&e->peds.score, n));
+    SFC_CUDA(dev_alloc(&e->peds.won, n));
+    SFC_CUDA(dev_alloc(&e->peds.moved_dir, n));
+    e->peds.n = n;
+    e->ped_capacity = n;
+    return SFC_OK;
+}
+
+int ensure_moved(sfc_engine* e, long long ticks) {
+    if (ticks <= e->moved_capacity) return SFC_OK;
+    cudaFree(e->moved_counts);
+    e->moved_counts = nullptr;
+    e->graph_valid = false;
+    const long long cap = std::max<long long>(ticks, 4096);
+    SFC_CUDA(dev_alloc(&e->moved_counts, cap));
+    e->moved_capacity = cap;
+    return SFC_OK;
+}
+
+int ensure_stage(sfc_engine* e) {
+    if (e->stage) return SFC_OK;
+    e->stage_cells = std::min<long long>(e->cells, kStageCells);
+    SFC_CUDA(dev_alloc(&e->stage, e->stage_cells * kSects));
+    return SFC_OK;
+}
+
+int ensure_debug(sfc_engine* e) {
+    if (e->dbg.enroll_ids) return SFC_OK;
+    const long long c = e->cells;
+    SFC_CUDA(dev_alloc(&e->dbg.enroll_ids, c * 8));
+    SFC_CUDA(dev_alloc(&e->dbg.enroll_scores, c * 8));
+    SFC_CUDA(dev_alloc(&e->dbg.winners, c));
+    SFC_CUDA(dev_alloc(&e->dbg.moved_from, c));
+    SFC_CUDA(dev_alloc(&e->dbg.moved_to, c));
+    SFC_CUDA(dev_alloc(&e->dbg.from_mask, c * 3));
+    SFC_CUDA(dev_alloc(&e->dbg.to_mask, c * 3));
+    e->dbg.cells = c;
+    SFC_CUDA(launch_dbg_clear(e->stream, e->dbg));
+    e->counters.kernel_launches += 1;
+    return SFC_OK;
+}
+
+// Pulls the control block back and converts a device-side error into the ABI status.
+int check_device_error(sfc_engine* e) {
+    Ctl h;
+    SFC_CUDA(cudaMemcpyAsync(&h, e->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    SFC_CUDA(cudaStreamSynchronize(e->stream));
+    e->tick = h.tick;
+    if (h.error_code == 0) return SFC_OK;
+    e->err_tick = h.error_tick;
+    e->err_phase = h.error_phase;
+    e->err_x = h.error_x;
+    e->err_y = h.error_y;
+    e->err_value = h.error_value;
+    char buf[256];
+    if (h.error_code == SFC_E_INTEGRITY && h.error_phase == 2) {
+        std::snprintf(buf, sizeof buf, "enrollment slot conflict at su (%d,%d)", h.error_x, h.error_y);
+    } else if (h.error_code == SFC_E_INTEGRITY && h.error_phase == 5) {
+        static const char* names[3] = {"dir-attractive", "dir-repulsive", "recurrent-repulsive"};
+        std::snprintf(buf, sizeof buf, "%s image drifted by %s", names[std::clamp(h.error_x, 0, 2)],
+                      std::to_string((float)h.error_value).c_str());
+    } else {
+        std::snprintf(buf, sizeof buf, "device error %d in phase %d (rebuild list capacity exceeded: %g centres)",
+                      h.error_code, h.error_phase, h.error_value);
+    }
+    e->err = buf;
+    return h.error_code;
+}
+
+K5Launch k5_args(sfc_engine* e, int advance) {
+    K5Launch l;
+    l.g = e->g;
+    l.t = e->tabs;
+    l.dyn = e->dyn;
+    l.ev = e->ev;
+    l.ctl = e->ctl;
+    l.chunk_k = e->cfg.chunk_k;
+    l.advance_tick = advance;
+    return l;
+}
+
+int enqueue_tick_kernels(sfc_engine* e) {
+    const DebugArrays none{};
+    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+    SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
+    SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none));
+    SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
+    return SFC_OK;
+}
+
+int enqueue_rebuild(sfc_engine* e) { // maybe_rebuild body, engine.cpp:540-549
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 1, 0.0));
+    SFC_CUDA(launch_drift_verdict(e->stream, e->ctl, e->cfg.rebuild_tolerance));
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 2, 0.0));
+    e->counters.kernel_launches += 3;
+    return SFC_OK;
+}
+
+int build_graph(sfc_engine* e) {
+    if (e->graph_valid) return SFC_OK;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    SFC_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_tick_kernels(e);
+    cudaError_t c = cudaStreamEndCapture(e->stream, &graph);
+    if (rc != SFC_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (c != cudaSuccess) return cuda_fail(e, c, "cudaStreamEndCapture");
+    c = cudaGraphInstantiate(&e->graph, graph, 0);
+    cudaGraphDestroy(graph);
+    if (c != cudaSuccess) return cuda_fail(e, c, "cudaGraphInstantiate");
+    e->graph_valid = true;
+    return SFC_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int sfc_abi_version(void) { return SFC_ABI_VERSION; }
+
+int sfc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out, char* err, size_t errlen) {
+    auto report = [&](int code, const std::string& msg) {
+        if (err && errlen) std::snprintf(err, errlen, "%s", msg.c_str());
+        return code;
+    };
+    *out = nullptr;
+    // Engine::Engine validation (engine.cpp:173-174), then the device-side limits
+    if (!(cfg->chunk_k == 2 || cfg->chunk_k == 4 || cfg->chunk_k == 8 || cfg->chunk_k == 16))
+        return report(SFC_E_CONFIG, "chunk_k: must be 2, 4, 8, or 16");
+    if (cfg->density_radius < 0) return report(SFC_E_CONFIG, "density_radius: must be >= 0");
+    if (cfg->width < 1) return report(SFC_E_CONFIG, "width: must be >= 1");
+    if (cfg->height < 1) return report(SFC_E_CONFIG, "height: must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+        return report(SFC_E_NO_DEVICE, "no CUDA device: the socfield B200 engine has no CPU fallback");
+    if (cfg->device < 0 || cfg->device >= ndev) return report(SFC_E_CONFIG, "device: ordinal out of range");
+
+    sfc_engine* e = new (std::nothrow) sfc_engine();
+    if (!e) return report(SFC_E_NOMEM, "out of host memory");
+    auto bail = [&](int code) {
+        const std::string msg = e->err;
+        sfc_destroy(e);
+        return report(code, msg);
+    };
+    e->cfg = *cfg;
+    e->device = cfg->device;
+    if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
+    e->g.W = cfg->width;
+    e->g.H = cfg->height;
+    e->g.closed = cfg->closed ? 1 : 0;
+    e->g.row0 = cfg->slab_rows > 0 ? cfg->slab_row0 : 0;
+    e->g.rows = cfg->slab_rows > 0 ? cfg->slab_rows : cfg->height;
+    e->g.halo = 0;
+    if (e->g.rows != cfg->height) return bail(fail(e, SFC_E_CONFIG, "slab_rows: partial slabs are not enabled in this build"));
+    e->dp.w_static = cfg->weight_static;
+    e->dp.w_kind[0] = cfg->weight_dir_attractive;
+    e->dp.w_kind[1] = cfg->weight_dir_repulsive;
+    e->dp.w_kind[2] = cfg->weight_recurrent;
+    e->dp.goal_bias = cfg->goal_bias;
+    e->dp.regulated = cfg->regulation != 0;
+    e->dp.density_radius = cfg->density_radius;
+    e->dp.fault_invert = cfg->fault_invert_vote_tiebreak != 0;
+
+    int rc = SFC_OK;
+    e->tabs.max_hw = e->tabs.max_hh = 0;
+    e->tabs.total_entries = 0;
+    for (int k = 0; k < kKinds && rc == SFC_OK; ++k) {
+        rc = upload_table(e, tables->kind[k], &e->tabs.k[k]);
+        if (rc == SFC_OK) {
+            e->tabs.max_hw = std::max(e->tabs.max_hw, e->tabs.k[k].hw);
+            e->tabs.max_hh = std::max(e->tabs.max_hh, e->tabs.k[k].hh);
+            e->tabs.total_entries += e->tabs.k[k].fw * e->tabs.k[k].fh;
+        }
+    }
+    if (rc != SFC_OK) return bail(rc);
+
+    auto cu = [&](cudaError_t c, const char* what) {
+        if (c != cudaSuccess && rc == SFC_OK) rc = cuda_fail(e, c, what);
+    };
+    e->cells = (long long)(e->g.rows + 2 * e->g.halo) * e->g.W;
+    cu(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cu(cudaEventCreate(&e->ev_start), "cudaEventCreate");
+    cu(cudaEventCreate(&e->ev_stop), "cudaEventCreate");
+    cu(dev_alloc(&e->occ, e->cells), "cudaMalloc(occupancy)");
+    cu(dev_alloc(&e->stat, e->cells * kSects), "cudaMalloc(static image)");
+    cu(dev_alloc(&e->dyn, e->cells * kKinds * kSects), "cudaMalloc(dynamic images)");
+    cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
+    cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
+    if (rc != SFC_OK) return bail(rc);
+    cu(cudaMemset(e->ctl, 0, sizeof(Ctl)), "cudaMemset");
+    cu(cudaMemset(e->occ, 0xFF, sizeof(int) * (size_t)e->cells), "cudaMemset");
+    cu(cudaMemset(e->stat, 0, sizeof(float) * (size_t)e->cells * kSects), "cudaMemset");
+    cu(cudaMemset(e->dyn, 0, sizeof(float) * (size_t)e->cells * kKinds * kSects), "cudaMemset");
+    cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
+    cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
+    cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
+    if (rc == SFC_OK) rc = ensure_peds(e, 0);
+    if (rc == SFC_OK) rc = ensure_moved(e, 1);
+    if (rc != SFC_OK) return bail(rc);
+    *out = e;
+    return SFC_OK;
+}
+
+void sfc_destroy(sfc_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    for (void* p : e->table_allocs) cudaFree(p);
+    free_peds(e);
+    cudaFree(e->occ);
+    cudaFree(e->stat);
+    cudaFree(e->dyn);
+    cudaFree(e->ev);
+    cudaFree(e->ctl);
+    cudaFree(e->moved_counts);
+    cudaFree(e->stage);
+    cudaFree(e->dbg.enroll_ids);
+    cudaFree(e->dbg.enroll_scores);
+    cudaFree(e->dbg.winners);
+    cudaFree(e->dbg.moved_from);
+    cudaFree(e->dbg.moved_to);
+    cudaFree(e->dbg.from_mask);
+    cudaFree(e->dbg.to_mask);
+    if (e->ev_start) cudaEventDestroy(e->ev_start);
+    if (e->ev_stop) cudaEventDestroy(e->ev_stop);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+const char* sfc_last_error(const sfc_engine* e) { return e ? e->err.c_str() : "null engine"; }
+
+void sfc_error_detail(const sfc_engine* e, int64_t* tick, int32_t* phase, int32_t* su_x, int32_t* su_y,
+                      double* value) {
+    if (tick) *tick = e->err_tick;
+    if (phase) *phase = e->err_phase;
+    if (su_x) *su_x = e->err_x;
+    if (su_y) *su_y = e->err_y;
+    if (value) *value = e->err_value;
+}
+
+int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
+    SFC_CUDA(cudaSetDevice(e->device));
+    const long long C = e->cells, P = v->n_peds;
+    int rc = ensure_peds(e, P);
+    if (rc != SFC_OK) return rc;
+    rc = ensure_stage(e);
+    if (rc != SFC_OK) return rc;
+    // pedestrian attributes: pack on the host (cheap, one pass), copy once
+    std::vector<int2> gate((size_t)P);
+    std::vector<uint32_t> attr((size_t)P);
+    for (long long i = 0; i < P; ++i) {
+        const int hw = (v->foot_w[i] - 1) / 2, hh = (v->foot_h[i] - 1) / 2;
+        if (hw > kMaxHalfExtent || hh > kMaxHalfExtent || hw < 0 || hh < 0)
+            return fail(e, SFC_E_CONFIG, "footprint: pedestrian footprint exceeds the device limit (4095)");
+        gate[(size_t)i] = make_int2(v->walk_period[i], v->walk_phase[i]);
+        attr[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
+    }
+    SFC_CUDA(cudaMemcpyAsync(e->occ, v->occupancy, sizeof(int) * (size_t)C, cudaMemcpyHostToDevice, e->stream));
+    SFC_CUDA(cudaMemcpyAsync(e->stat, v->static_image, sizeof(float) * (size_t)C * kSects, cudaMemcpyHostToDevice, e->stream));
+    e->counters.h2d_bytes += (int64_t)(sizeof(int) * C + sizeof(float) * C * kSects);
+    for (int k = 0; k < kKinds; ++k) {
+        for (long long c0 = 0; c0 < C; c0 += e->stage_cells) {
+            const long long n = std::min(e->stage_cells, C - c0);
+            SFC_CUDA(cudaMemcpyAsync(e->stage, v->dyn_images[k] + c0 * kSects, sizeof(float) * (size_t)n * kSects,
+                                     cudaMemcpyHostToDevice, e->stream));
+            SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, c0, n));
+            e->counters.kernel_launches += 1;
+            e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
+        }
+    }
+    if (P > 0) {
+        SFC_CUDA(cudaMemcpyAsync(e->peds.center, v->center_xy, sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemcpyAsync(e->peds.gate, gate.data(), sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemcpyAsync(e->peds.attr, attr.data(), sizeof(uint32_t) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.dir, 0xFF, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.moved_dir, 0xFF, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.won, 0, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.score, 0, sizeof(double) * (size_t)P, e->stream));
+        e->counters.h2d_bytes += (int64_t)((sizeof(int2) * 2 + sizeof(uint32_t)) * P);
+    }
+    SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
+    Ctl h{};
+    h.tick = v->tick;
+    h.run_base = v->tick;
+    SFC_CUDA(cudaMemcpyAsync(e->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, e->stream));
+    SFC_CUDA(cudaStreamSynchronize(e->stream)); // gate/attr staging vectors die here
+    e->tick = v->tick;
+    e->uploaded = true;
+    return SFC_OK;
+}
+
+int sfc_download(sfc_engine* e, sfc_state_view* v) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "download before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    const long long C = e->cells, P = e->peds.n;
+    int rc = ensure_stage(e);
+    if (rc != SFC_OK) return rc;
+    if (v->occupancy) {
+        SFC_CUDA(cudaMemcpyAsync(v->occupancy, e->occ, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost, e->stream));
+        e->counters.d2h_bytes += (int64_t)(sizeof(int) * C);
+    }
+    for (int k = 0; k < kKinds; ++k) {
+        if (!v->dyn_images[k]) continue;
+        for (long long c0 = 0; c0 < C; c0 += e->stage_cells) {
+            const long long n = std::min(e->stage_cells, C - c0);
+            SFC_CUDA(launch_deinterleave(e->stream, e->dyn, e->stage, k, c0, n));
+            SFC_CUDA(cudaMemcpyAsync(v->dyn_images[k] + c0 * kSects, e->stage, sizeof(float) * (size_t)n * kSects,
+                                     cudaMemcpyDeviceToHost, e->stream));
+            SFC_CUDA(cudaStreamSynchronize(e->stream)); // staging buffer is reused by the next chunk
+            e->counters.kernel_launches += 1;
+            e->counters.d2h_bytes += (int64_t)(sizeof(float) * n * kSects);
+        }
+    }
+    if (v->static_image) {
+        SFC_CUDA(cudaMemcpyAsync(v->static_image, e->stat, sizeof(float) * (size_t)C * kSects, cudaMemcpyDeviceToHost, e->stream));
+        e->counters.d2h_bytes += (int64_t)(sizeof(float) * C * kSects);
+    }
+    if (v->center_xy && P > 0) {
+        SFC_CUDA(cudaMemcpyAsync(v->center_xy, e->peds.center, sizeof(int2) * (size_t)P, cudaMemcpyDeviceToHost, e->stream));
+        e->counters.d2h_bytes += (int64_t)(sizeof(int2) * P);
+    }
+    rc = check_device_error(e); // also refreshes e->tick
+    v->tick = e->tick;
+    v->n_peds = P;
+    (void)rc; // the state is valid to read even after a recorded integrity error
+    return SFC_OK;
+}
+
+int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_phase_times) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "run before upload");
+    if (ticks <= 0) return SFC_OK;
+    SFC_CUDA(cudaSetDevice(e->device));
+    int rc = ensure_moved(e, ticks);
+    if (rc != SFC_OK) return rc;
+    SFC_CUDA(cudaMemsetAsync(e->moved_counts, 0, sizeof(unsigned long long) * (size_t)ticks, e->stream));
+    const long long base = e->tick;
+    SFC_CUDA(cudaMemcpyAsync(&e->ctl->run_base, &base, sizeof(long long), cudaMemcpyHostToDevice, e->stream));
+    const long long interval = e->cfg.rebuild_interval;
+
+    std::vector<cudaEvent_t> evs;
+    if (with_phase_times) {
+        evs.resize((size_t)ticks * 5 + 1);
+        for (auto& x : evs) SFC_CUDA(cudaEventCreate(&x));
+    } else {
+        rc = build_graph(e);
+        if (rc != SFC_OK) return rc;
+    }
+    SFC_CUDA(cudaEventRecord(e->ev_start, e->stream));
+    for (long long t = 0; t < ticks; ++t) {
+        if (with_phase_times) {
+            const DebugArrays none{};
+            cudaEvent_t* ev = &evs[(size_t)t * 5];
+            SFC_CUDA(cudaEventRecord(ev[0], e->stream));
+            // k-1 has no device work: its slot reports zero
+            SFC_CUDA(cudaEventRecord(ev[1], e->stream));
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+            SFC_CUDA(cudaEventRecord(ev[2], e->stream));
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
+            SFC_CUDA(cudaEventRecord(ev[3], e->stream));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none));
+            SFC_CUDA(cudaEventRecord(ev[4], e->stream));
+            SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
+            if (t == ticks - 1) SFC_CUDA(cudaEventRecord(evs[(size_t)ticks * 5], e->stream));
+        } else {
+            SFC_CUDA(cudaGraphLaunch(e->graph, e->stream));
+            e->counters.graph_launches += 1;
+        }
+        e->counters.kernel_launches += 4;
+        if (interval > 0 && (base + t + 1) % interval == 0) {
+            rc = enqueue_rebuild(e);
+            if (rc != SFC_OK) return rc;
+        }
+    }
+    SFC_CUDA(cudaEventRecord(e->ev_stop, e->stream));
+    std::vector<unsigned long long> moved;
+    if (metrics) {
+        moved.resize((size_t)ticks);
+        SFC_CUDA(cudaMemcpyAsync(moved.data(), e->moved_counts, sizeof(unsigned long long) * (size_t)ticks,
+                                 cudaMemcpyDeviceToHost, e->stream));
+    }
+    rc = check_device_error(e); // synchronises
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
+    e->last_run_ms = ms;
+    if (metrics) {
+        for (long long t = 0; t < ticks; ++t) {
+            sfc_tick_metrics& m = metrics[t];
+            m.tick = base + t;
+            m.moved = (int64_t)moved[(size_t)t];
+            for (int p = 0; p < 5; ++p) m.phase_us[p] = 0;
+            m.wall_us = (int64_t)(ms * 1000.0 / (double)ticks);
+            if (with_phase_times) {
+                for (int p = 0; p < 5; ++p) {
+                    float pm = 0.0f;
+                    cudaEvent_t next = p < 4 ? evs[(size_t)t * 5 + p + 1]
+                                             : (t + 1 < ticks ? evs[(size_t)(t + 1) * 5] : evs[(size_t)ticks * 5]);
+                    cudaEventElapsedTime(&pm, evs[(size_t)t * 5 + p], next);
+                    m.phase_us[p] = (int64_t)(pm * 1000.0f);
+                }
+                m.wall_us = m.phase_us[0] + m.phase_us[1] + m.phase_us[2] + m.phase_us[3] + m.phase_us[4];
+            }
+        }
+    }
+    for (auto& x : evs) cudaEventDestroy(x);
+    return rc;
+}
+
+int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "phase before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    int rc = ensure_debug(e);
+    if (rc != SFC_OK) return rc;
+    switch (phase) {
+        case 1: {
+            const long long base = e->tick;
+            SFC_CUDA(cudaMemcpyAsync(&e->ctl->run_base, &base, sizeof(long long), cudaMemcpyHostToDevice, e->stream));
+            SFC_CUDA(cudaMemsetAsync(e->moved_counts, 0, sizeof(unsigned long long), e->stream));
+            SFC_CUDA(launch_dbg_clear(e->stream, e->dbg));
+            e->counters.kernel_launches += 1;
+            break;
+        }
+        case 2:
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+            SFC_CUDA(launch_dbg_enroll(e->stream, e->g, e->peds, e->dbg, e->ctl));
+            e->counters.kernel_launches += 2;
+            break;
+        case 3:
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
+            SFC_CUDA(launch_dbg_vote(e->stream, e->dbg, e->dp.fault_invert));
+            e->counters.kernel_launches += 2;
+            break;
+        case 4:
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, e->dbg));
+            e->counters.kernel_launches += 1;
+            break;
+        case 5:
+            SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 0)));
+            e->counters.kernel_launches += 1;
+            break;
+        case 6: {
+            SFC_CUDA(launch_tick_advance(e->stream, e->ctl));
+            e->counters.kernel_launches += 1;
+            const long long interval = e->cfg.rebuild_interval;
+            if (interval > 0 && (e->tick + 1) % interval == 0) {
+                rc = enqueue_rebuild(e);
+                if (rc != SFC_OK) return rc;
+            }
+            break;
+        }
+        default: return fail(e, SFC_E_STATE, "phase must be 1..6");
+    }
+    if (moved) {
+        unsigned long long m = 0;
+        SFC_CUDA(cudaMemcpyAsync(&m, e->moved_counts, sizeof m, cudaMemcpyDeviceToHost, e->stream));
+        SFC_CUDA(cudaStreamSynchronize(e->stream));
+        *moved = (int64_t)m;
+    }
+    return check_device_error(e);
+}
+
+int sfc_download_temporaries(sfc_engine* e, sfc_temporaries* out) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "download before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    int rc = ensure_debug(e);
+    if (rc != SFC_OK) return rc;
+    const long long C = e->cells, P = e->peds.n;
+    SFC_CUDA(cudaStreamSynchronize(e->stream));
+    if (out->decisions && P > 0) {
+        std::vector<int8_t> d((size_t)P);
+        SFC_CUDA(cudaMemcpy(d.data(), e->peds.dir, (size_t)P, cudaMemcpyDeviceToHost));
+        for (long long i = 0; i < P; ++i) out->decisions[i] = d[(size_t)i];
+    }
+    if (out->decision_scores && P > 0)
+        SFC_CUDA(cudaMemcpy(out->decision_scores, e->peds.score, sizeof(double) * (size_t)P, cudaMemcpyDeviceToHost));
+    if (out->enroll_ids) SFC_CUDA(cudaMemcpy(out->enroll_ids, e->dbg.enroll_ids, sizeof(int) * (size_t)C * 8, cudaMemcpyDeviceToHost));
+    if (out->enroll_scores)
+        SFC_CUDA(cudaMemcpy(out->enroll_scores, e->dbg.enroll_scores, sizeof(double) * (size_t)C * 8, cudaMemcpyDeviceToHost));
+    if (out->winners) SFC_CUDA(cudaMemcpy(out->winners, e->dbg.winners, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost));
+    if (out->moved_from) SFC_CUDA(cudaMemcpy(out->moved_from, e->dbg.moved_from, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost));
+    if (out->moved_to) SFC_CUDA(cudaMemcpy(out->moved_to, e->dbg.moved_to, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost));
+    if (out->from_mask) SFC_CUDA(cudaMemcpy(out->from_mask, e->dbg.from_mask, (size_t)C * 3, cudaMemcpyDeviceToHost));
+    if (out->to_mask) SFC_CUDA(cudaMemcpy(out->to_mask, e->dbg.to_mask, (size_t)C * 3, cudaMemcpyDeviceToHost));
+    return SFC_OK;
+}
+
+int sfc_decide(sfc_engine* e, int64_t ped, int32_t* direction, double* score) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "decide before upload");
+    if (ped < 0 || ped >= e->peds.n) return fail(e, SFC_E_STATE, "pedestrian index out of range");
+    SFC_CUDA(cudaSetDevice(e->device));
+    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+    e->counters.kernel_launches += 1;
+    int8_t d = -1;
+    SFC_CUDA(cudaMemcpyAsync(&d, e->peds.dir + ped, 1, cudaMemcpyDeviceToHost, e->stream));
+    SFC_CUDA(cudaMemcpyAsync(score, e->peds.score + ped, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    SFC_CUDA(cudaStreamSynchronize(e->stream));
+    *direction = d;
+    return SFC_OK;
+}
+
+int sfc_rasterize_dynamic(sfc_engine* e, float* out[SFC_KINDS]) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "rasterize before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    int rc = ensure_stage(e);
+    if (rc != SFC_OK) return rc;
+    float* scratch = nullptr;
+    SFC_CUDA(dev_alloc(&scratch, e->cells * kKinds * kSects));
+    cudaError_t c = launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, scratch, e->ctl, 0, 0.0);
+    e->counters.kernel_launches += 1;
+    for (int k = 0; k < kKinds && c == cudaSuccess; ++k) {
+        for (long long c0 = 0; c0 < e->cells && c == cudaSuccess; c0 += e->stage_cells) {
+            const long long n = std::min(e->stage_cells, e->cells - c0);
+            c = launch_deinterleave(e->stream, scratch, e->stage, k, c0, n);
+            if (c == cudaSuccess)
+                c = cudaMemcpyAsync(out[k] + c0 * kSects, e->stage, sizeof(float) * (size_t)n * kSects, cudaMemcpyDeviceToHost, e->stream);
+            if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+            e->counters.kernel_launches += 1;
+        }
+    }
+    cudaFree(scratch);
+    if (c != cudaSuccess) return cuda_fail(e, c, "sfc_rasterize_dynamic");
+    return check_device_error(e);
+}
+
+int sfc_reset_dynamic_images(sfc_engine* e) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "rasterize before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 2, 0.0));
+    e->counters.kernel_launches += 1;
+    return check_device_error(e);
+}
+
+int sfc_rasterize_static(sfc_engine* e, int32_t n_tables, const sfc_kind_table* tables, int64_t n_anchors,
+                         const sfc_anchor* anchors, const float* base, float* out) {
+    SFC_CUDA(cudaSetDevice(e->device));
+    std::vector<KindTableDev> dev((size_t)std::max(n_tables, 1));
+    const size_t first_alloc = e->table_allocs.size();
+    int rc = SFC_OK;
+    for (int t = 0; t < n_tables && rc == SFC_OK; ++t) rc = upload_table(e, tables[t], &dev[(size_t)t]);
+    if (rc == SFC_OK) {
+        cudaError_t c = base ? cudaMemcpyAsync(e->stat, base, sizeof(float) * (size_t)e->cells * kSects,
+                                               cudaMemcpyHostToDevice, e->stream)
+                             : cudaMemsetAsync(e->stat, 0, sizeof(float) * (size_t)e->cells * kSects, e->stream);
+        for (int64_t i = 0; i < n_anchors && c == cudaSuccess; ++i) { // list order = stream order
+            if (anchors[i].table < 0 || anchors[i].table >= n_tables) {
+                rc = fail(e, SFC_E_CONFIG, "anchor: table index out of range");
+                break;
+            }
+            c = launch_static_anchor(e->stream, e->g, dev[(size_t)anchors[i].table], e->stat, anchors[i].x, anchors[i].y,
+                                     anchors[i].orientation);
+            e->counters.kernel_launches += 1;
+        }
+        if (c == cudaSuccess && out && rc == SFC_OK)
+            c = cudaMemcpyAsync(out, e->stat, sizeof(float) * (size_t)e->cells * kSects, cudaMemcpyDeviceToHost, e->stream);
+        if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+        if (c != cudaSuccess) rc = cuda_fail(e, c, "sfc_rasterize_static");
+    }
+    for (size_t i = first_alloc; i < e->table_allocs.size(); ++i) cudaFree(e->table_allocs[i]);
+    e->table_allocs.resize(first_alloc);
+    return rc;
+}
+
+void sfc_get_counters(const sfc_engine* e, sfc_counters* out) { *out = e->counters; }
+
+double sfc_last_run_ms(const sfc_engine* e) { return e->last_run_ms; }
+
+} // extern "C"

@@ -1,0 +1,197 @@
+// sfc_internal.cuh — device-side data model shared by the sm_100a kernels.
+//
+// HBM layout (one engine = one row slab of the SU grid, normally the whole grid):
+//   occ   int32 [rows_local][W]            occupant id per su, -1 empty        (grid.hpp:94-116)
+//   stat  float [rows_local][W][8]         static strength image               (fields.hpp:89-112)
+//   dyn   float [rows_local][W][3][8]      the three dynamic images INTERLEAVED per su: one
+//                                          96-byte record, so the k-5 read-modify-write and the
+//                                          k-2 centre read are single contiguous runs
+//   ev    uint8 [rows_local][W][2]         movement events of the current tick (replaces the
+//                                          reference's 14-byte MovementLog, engine.hpp:81-89):
+//                                          byte 0 = "a pedestrian left this centre", byte 1 =
+//                                          "arrived"; 0x80 | orient_attr | orient_rep << 3
+//   per pedestrian (SoA): centre int2, gate int2 (period, phase), attr u32, decision dir int8 +
+//   score f64, vote result u8, direction of the previous tick's move int8.
+// rows_local = slab_rows + 2 * halo; the whole-grid engine has halo 0.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "socfield_cuda.h"
+
+namespace sfc {
+
+constexpr int kSects = 8;
+constexpr int kKinds = 3;
+constexpr int kStill = -1;
+constexpr int kNoPed = -1;
+
+struct GridDev {
+    int W, H;      // global extent
+    int closed;    // BoundaryMode::Closed
+    int row0;      // first owned global row
+    int rows;      // owned rows
+    int halo;      // resident rows beyond each slab edge
+};
+
+// Euclidean modulo (grid.cpp:8-11).
+__host__ __device__ __forceinline__ int emod(int a, int m) {
+    if (a >= 0 && a < m) return a;
+    int r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// Local flat su index of unwrapped global coordinates, or -1 when the su does not exist
+// (closed boundary, grid.cpp:15-21) or is not resident in this slab.
+__host__ __device__ __forceinline__ long long cell_index(const GridDev& g, int x, int y) {
+    if (g.closed) {
+        if (x < 0 || x >= g.W || y < 0 || y >= g.H) return -1;
+    } else {
+        x = emod(x, g.W);
+        y = emod(y, g.H);
+    }
+    int ly = y - g.row0;
+    if (!g.closed) ly = emod(ly + g.halo, g.H) - g.halo;
+    if (ly < -g.halo || ly >= g.rows + g.halo) return -1;
+    return (long long)(ly + g.halo) * g.W + x;
+}
+
+__host__ __device__ __forceinline__ bool row_owned(const GridDev& g, int y) {
+    int ly = y - g.row0;
+    if (!g.closed) ly = emod(ly, g.H);
+    return ly >= 0 && ly < g.rows;
+}
+
+// sect_step (fields.cpp:67-72) without a table: sect 0 = +x, counter-clockwise.
+__host__ __device__ __forceinline__ int step_dx(int sect) {
+    return (sect == 0 || sect == 1 || sect == 7) ? 1 : ((sect >= 3 && sect <= 5) ? -1 : 0);
+}
+__host__ __device__ __forceinline__ int step_dy(int sect) {
+    return (sect >= 1 && sect <= 3) ? 1 : ((sect >= 5) ? -1 : 0);
+}
+
+// attr word of a pedestrian
+__host__ __device__ __forceinline__ uint32_t pack_attr(int goal, int o_att, int o_rep, int half_w, int half_h) {
+    return (uint32_t)goal | ((uint32_t)o_att << 3) | ((uint32_t)o_rep << 6) | ((uint32_t)half_w << 9) |
+           ((uint32_t)half_h << 20);
+}
+__host__ __device__ __forceinline__ int attr_goal(uint32_t a) { return a & 7; }
+__host__ __device__ __forceinline__ int attr_orient(uint32_t a, int kind) { return (a >> (3 + 3 * kind)) & 7; }
+__host__ __device__ __forceinline__ int attr_half_w(uint32_t a) { return (a >> 9) & 0x7FF; }
+__host__ __device__ __forceinline__ int attr_half_h(uint32_t a) { return (a >> 20) & 0x7FF; }
+constexpr int kMaxHalfExtent = 0x7FF;
+
+// event byte: 0x80 | orient(dir-attractive) | orient(dir-repulsive) << 3
+__host__ __device__ __forceinline__ uint8_t event_code(uint32_t attr) { return (uint8_t)(0x80u | ((attr >> 3) & 0x3Fu)); }
+
+struct PedArrays {
+    long long n;
+    int2* center;
+    int2* gate;       // (walk_period, walk_phase)
+    uint32_t* attr;
+    int8_t* dir;      // decision of the current tick (k-2)
+    double* score;
+    uint8_t* won;     // k-3 result: wins every newly covered su
+    int8_t* moved_dir; // direction moved in the previous tick, -1 none (for event clearing)
+};
+
+struct DecideParams {
+    double w_static, w_kind[kKinds], goal_bias;
+    int regulated;      // Regulation::Linear
+    int density_radius;
+    int fault_invert;
+};
+
+// Device-resident control block: lets a captured CUDA graph replay tick after tick with no
+// host-side parameter patching.
+struct Ctl {
+    long long tick;          // SimState::tick
+    long long run_base;      // tick at the start of the current sfc_run
+    int error_code;          // first error wins (atomicCAS)
+    int error_phase;
+    long long error_tick;
+    int error_x, error_y;
+    double error_value;
+    unsigned int drift_bits[kKinds]; // max |old - fresh| per kind as float bits (rebuild)
+    int pad;
+};
+
+// Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
+struct DebugArrays {
+    int32_t* enroll_ids;     // [C*8]
+    double* enroll_scores;   // [C*8]
+    int32_t* winners;        // [C]
+    int32_t* moved_from;     // [C]
+    int32_t* moved_to;       // [C]
+    uint8_t* from_mask;      // [3*C]
+    uint8_t* to_mask;        // [3*C]
+    long long cells;
+};
+
+struct KindTableDev {
+    int fw, fh, hw, hh;
+    const double* mag;     // [fh*fw]
+    const uint32_t* info;  // [fh*fw]
+};
+
+struct TablesDev {
+    KindTableDev k[kKinds];
+    int max_hw, max_hh;
+    int total_entries;
+};
+
+__device__ __forceinline__ void raise_error(Ctl* ctl, int code, int phase, int x, int y, double value) {
+    if (atomicCAS(&ctl->error_code, 0, code) == 0) {
+        ctl->error_phase = phase;
+        ctl->error_tick = ctl->tick;
+        ctl->error_x = x;
+        ctl->error_y = y;
+        ctl->error_value = value;
+    }
+}
+
+// ---- launchers (defined in the .cu files) --------------------------------------------------
+struct K5Launch {
+    GridDev g;
+    TablesDev t;
+    float* dyn;
+    const uint8_t* ev;
+    Ctl* ctl;
+    int chunk_k;
+    int advance_tick; // fold "tick += 1" into the kernel (fast path)
+};
+cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
+                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp);
+cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
+                           const DecideParams& dp);
+cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
+                           unsigned long long* moved_counts, const DebugArrays& dbg);
+cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& a);
+size_t k5_smem_bytes(int chunk_k, const TablesDev& t);
+
+// rebuild / rasterize_dynamic.  mode 0: write fresh images to `out` (record layout), no compare;
+// mode 1: compare with dyn and record the per-kind drift maxima in ctl; mode 2: overwrite dyn
+// unless ctl holds an error.
+cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
+                           float* dyn, float* out, Ctl* ctl, int mode, double tolerance);
+cudaError_t launch_drift_verdict(cudaStream_t s, Ctl* ctl, double tolerance);
+
+// debug materialisation of the reference's temporaries
+cudaError_t launch_dbg_clear(cudaStream_t s, const DebugArrays& d);
+cudaError_t launch_dbg_enroll(cudaStream_t s, const GridDev& g, const PedArrays& p, const DebugArrays& d, Ctl* ctl);
+cudaError_t launch_dbg_vote(cudaStream_t s, const DebugArrays& d, int fault_invert);
+
+// layout conversion between the host's per-kind images and the interleaved record buffer
+cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, int kind, long long cells_begin,
+                              long long cells);
+cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
+                                long long cells);
+cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v);
+cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl);
+cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,
+                                 int orientation);
+cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t);
+cudaError_t prepare_rebuild(const TablesDev& t);
+
+} // namespace sfc

@@ -1,0 +1,400 @@
+// sfc_ped_kernels.cu — per-pedestrian phases of the tick: k-2 decide, k-3 vote, k-4 move.
+//
+// k-2 follows the reference's decide_core arithmetic exactly (engine.cpp:289-324): double
+// precision, products and sums individually rounded (__dmul_rn/__dadd_rn — the reference binary
+// contains no FMA), the 19-comparator sort network with ties to the lower sect (engine.cpp:31-50).
+//
+// k-3/k-4 do NOT materialise the reference's 96-byte-per-su EnrollmentTable.  Under v_max = 1
+// the only pedestrian that can register for su c through slot d is the occupant of c - step(d)
+// (engine.hpp:45-48), so the winner test for a newly covered su is an 8-neighbour gather on
+// the occupancy grid plus the per-pedestrian decision arrays: same result, no per-su
+// temporaries, no atomics, no full-grid clear (the reference's k-1).
+
+#include "sfc_internal.cuh"
+
+namespace sfc {
+
+namespace {
+
+constexpr int kPedThreads = 128;
+
+__device__ __forceinline__ int sect_distance(int a, int b) { // fields.cpp:62-65
+    int d = (a - b) & 7;
+    return d < 8 - d ? d : 8 - d;
+}
+
+// Visits the su a step in `dir` would newly cover (engine.cpp:271-287: the cells of the new
+// footprint the old footprint does not already cover form an L: one column if the step has an
+// x component, one row if it has a y component).  fn(x, y) gets unwrapped global coordinates
+// and returns false to stop early.  Returns false if stopped.
+template <class Fn>
+__device__ __forceinline__ bool for_new_cells(int cx, int cy, int rw, int rh, int dir, Fn&& fn) {
+    const int ux = step_dx(dir), uy = step_dy(dir);
+    const int ncx = cx + ux, ncy = cy + uy;
+    if (ux != 0) {
+        const int ox = ux > 0 ? rw : -rw;
+        for (int oy = -rh; oy <= rh; ++oy)
+            if (!fn(ncx + ox, ncy + oy)) return false;
+    }
+    if (uy != 0) {
+        const int oy = uy > 0 ? rh : -rh;
+        const int skip = ux != 0 ? (ux > 0 ? rw : -rw) : (rw + 1); // corner already visited
+        for (int ox = -rw; ox <= rw; ++ox) {
+            if (ox == skip) continue;
+            if (!fn(ncx + ox, ncy + oy)) return false;
+        }
+    }
+    return true;
+}
+
+// One compare-exchange of the sort network on (score, sect) pairs: keep the better key first —
+// higher score, lower sect on ties (engine.cpp:34-41).
+__device__ __forceinline__ void cex(double& sa, int& ia, double& sb, int& ib) {
+    const bool swap = (sa < sb) || (sa == sb && ia > ib);
+    const double ts = swap ? sb : sa;
+    const int ti = swap ? ib : ia;
+    sb = swap ? sa : sb;
+    ib = swap ? ia : ib;
+    sa = ts;
+    ia = ti;
+}
+
+__global__ void __launch_bounds__(kPedThreads)
+k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const float* __restrict__ stat,
+                 const float* __restrict__ dyn, uint8_t* __restrict__ ev, Ctl* ctl, DecideParams dp) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    if (ctl->error_code != 0) return;
+    const int2 c = p.center[i];
+    if (!row_owned(g, c.y)) return;
+    const uint32_t attr = p.attr[i];
+
+    // Retire the previous tick's movement events of this pedestrian (the reference clears its
+    // whole MovementLog in k-1, engine.cpp:335-339; here only the two touched su are reset).
+    const int md = p.moved_dir[i];
+    if (md >= 0) {
+        const long long to = cell_index(g, c.x, c.y);
+        const long long from = cell_index(g, c.x - step_dx(md), c.y - step_dy(md));
+        ev[2 * to + 1] = 0;
+        if (from >= 0) ev[2 * from] = 0;
+        p.moved_dir[i] = -1;
+    }
+
+    int8_t out_dir = kStill;
+    double out_score = 0.0;
+
+    const int2 gate = p.gate[i];
+    const long long tick = ctl->tick;
+    if (tick % gate.x == gate.y) { // walk gate, engine.cpp:291
+        const int rw = attr_half_w(attr), rh = attr_half_h(attr);
+        double gfac = 1.0;
+        if (dp.regulated) { // local_density (grid.cpp:58-72) + regulate (engine.cpp:242-248)
+            int occupied = 0, window = 0;
+            const int r = dp.density_radius;
+            for (int oy = -r; oy <= r; ++oy) {
+                for (int ox = -r; ox <= r; ++ox) {
+                    const long long idx = cell_index(g, c.x + ox, c.y + oy);
+                    if (idx < 0) continue;
+                    ++window;
+                    occupied += occ[idx] != kNoPed;
+                }
+            }
+            const double rho = window == 0 ? 0.0 : __ddiv_rn((double)occupied, (double)window);
+            gfac = fmax(0.1, __dsub_rn(1.0, rho));
+        }
+
+        const long long base = cell_index(g, c.x, c.y);
+        const float4* sp = reinterpret_cast<const float4*>(stat + base * kSects);
+        const float4* dq = reinterpret_cast<const float4*>(dyn + base * (kKinds * kSects));
+        float img[4][8];
+        {
+            const float4 a = __ldg(sp), b = __ldg(sp + 1);
+            img[0][0] = a.x; img[0][1] = a.y; img[0][2] = a.z; img[0][3] = a.w;
+            img[0][4] = b.x; img[0][5] = b.y; img[0][6] = b.z; img[0][7] = b.w;
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                const float4 u = dq[2 * k], v = dq[2 * k + 1];
+                img[k + 1][0] = u.x; img[k + 1][1] = u.y; img[k + 1][2] = u.z; img[k + 1][3] = u.w;
+                img[k + 1][4] = v.x; img[k + 1][5] = v.y; img[k + 1][6] = v.z; img[k + 1][7] = v.w;
+            }
+        }
+        const int goal = attr_goal(attr);
+        double s[8];
+        int o[8];
+#pragma unroll
+        for (int sect = 0; sect < 8; ++sect) {
+            double raw = __dmul_rn(dp.w_static, (double)img[0][sect]);
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) raw = __dadd_rn(raw, __dmul_rn(dp.w_kind[k], (double)img[k + 1][sect]));
+            const int dist = sect_distance(sect, goal);
+            const double kcos = dist == 0 ? 1.0 : (dist == 1 ? 0.70710678118654752440 : 0.0);
+            s[sect] = __dadd_rn(__dmul_rn(gfac, raw), __dmul_rn(dp.goal_bias, kcos));
+            o[sect] = sect;
+        }
+        // sort8_desc, engine.cpp:42-48
+        cex(s[0], o[0], s[1], o[1]); cex(s[2], o[2], s[3], o[3]); cex(s[0], o[0], s[2], o[2]);
+        cex(s[1], o[1], s[3], o[3]); cex(s[1], o[1], s[2], o[2]);
+        cex(s[4], o[4], s[5], o[5]); cex(s[6], o[6], s[7], o[7]); cex(s[4], o[4], s[6], o[6]);
+        cex(s[5], o[5], s[7], o[7]); cex(s[5], o[5], s[6], o[6]);
+        cex(s[0], o[0], s[4], o[4]); cex(s[1], o[1], s[5], o[5]); cex(s[1], o[1], s[4], o[4]);
+        cex(s[2], o[2], s[6], o[6]); cex(s[3], o[3], s[7], o[7]); cex(s[3], o[3], s[6], o[6]);
+        cex(s[2], o[2], s[4], o[4]); cex(s[3], o[3], s[5], o[5]); cex(s[3], o[3], s[4], o[4]);
+
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (out_dir != kStill) break;
+            if (s[r] <= 0.0) break; // sorted: no later direction qualifies (engine.cpp:319)
+            const bool ok = for_new_cells(c.x, c.y, rw, rh, o[r], [&](int x, int y) {
+                const long long idx = cell_index(g, x, y);
+                return idx >= 0 && occ[idx] == kNoPed; // move_cells_empty, engine.cpp:256-269
+            });
+            if (ok) {
+                out_dir = (int8_t)o[r];
+                out_score = s[r];
+            }
+        }
+    }
+    p.dir[i] = out_dir;
+    p.score[i] = out_score;
+}
+
+__global__ void __launch_bounds__(kPedThreads)
+k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    if (ctl->error_code != 0) return;
+    const int d = p.dir[i];
+    if (d < 0) return;
+    const int2 c = p.center[i];
+    if (!row_owned(g, c.y)) return;
+    const uint32_t attr = p.attr[i];
+    const double my = p.score[i];
+    // engine.cpp:365-386 restated per claimant: I win su c iff no other registrant of c beats
+    // (score, then lower id — higher id under the fault hook).
+    const bool won = for_new_cells(c.x, c.y, attr_half_w(attr), attr_half_h(attr), d, [&](int x, int y) {
+#pragma unroll
+        for (int slot = 0; slot < 8; ++slot) {
+            const long long idx = cell_index(g, x - step_dx(slot), y - step_dy(slot));
+            if (idx < 0) continue;
+            const int q = occ[idx];
+            if (q < 0 || q == (int)i) continue;
+            if (p.dir[q] != slot) continue;
+            const double theirs = p.score[q];
+            if (theirs > my) return false;
+            if (theirs == my && (fault ? q > (int)i : q < (int)i)) return false;
+        }
+        return true;
+    });
+    p.won[i] = won ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kPedThreads)
+k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restrict__ ev, Ctl* ctl,
+               unsigned long long* __restrict__ moved_counts, DebugArrays dbg) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool moved = false;
+    if (i < p.n && ctl->error_code == 0) {
+        const int d = p.dir[i];
+        const int2 c = p.center[i];
+        if (d >= 0 && p.won[i] && row_owned(g, c.y)) {
+            const uint32_t attr = p.attr[i];
+            const int rw = attr_half_w(attr), rh = attr_half_h(attr);
+            const int ux = step_dx(d), uy = step_dy(d);
+            // release the su the new footprint no longer covers (engine.cpp:403-409): the mirror
+            // image of the newly covered L, taken around the old centre
+            if (ux != 0) {
+                const int ox = ux > 0 ? -rw : rw;
+                for (int oy = -rh; oy <= rh; ++oy) {
+                    const long long idx = cell_index(g, c.x + ox, c.y + oy);
+                    if (idx >= 0) occ[idx] = kNoPed;
+                }
+            }
+            if (uy != 0) {
+                const int oy = uy > 0 ? -rh : rh;
+                for (int ox = -rw; ox <= rw; ++ox) {
+                    const long long idx = cell_index(g, c.x + ox, c.y + oy);
+                    if (idx >= 0) occ[idx] = kNoPed;
+                }
+            }
+            for_new_cells(c.x, c.y, rw, rh, d, [&](int x, int y) { // engine.cpp:410
+                const long long idx = cell_index(g, x, y);
+                if (idx >= 0) occ[idx] = (int)i;
+                return true;
+            });
+            int nx = c.x + ux, ny = c.y + uy;
+            if (!g.closed) {
+                nx = emod(nx, g.W);
+                ny = emod(ny, g.H);
+            }
+            p.center[i] = make_int2(nx, ny);
+            const long long from = cell_index(g, c.x, c.y), to = cell_index(g, nx, ny);
+            const uint8_t code = event_code(attr);
+            ev[2 * from] = code;
+            if (to >= 0) ev[2 * to + 1] = code;
+            p.moved_dir[i] = (int8_t)d;
+            if (dbg.moved_from) { // MovementLog as the reference shapes it (engine.cpp:412-423)
+                dbg.moved_from[from] = (int)i;
+                dbg.moved_to[to] = (int)i;
+                for (int k = 0; k < kKinds; ++k) {
+                    const uint8_t mask = k < 2 ? (uint8_t)(1u << attr_orient(attr, k)) : (uint8_t)0xFF;
+                    dbg.from_mask[(long long)k * dbg.cells + from] = mask;
+                    dbg.to_mask[(long long)k * dbg.cells + to] = mask;
+                }
+            }
+            moved = true;
+        }
+    }
+    // TickMetrics::moved: one atomic per warp
+    const unsigned ballot = __ballot_sync(0xFFFFFFFFu, moved);
+    if ((threadIdx.x & 31) == 0 && ballot != 0) {
+        atomicAdd(&moved_counts[ctl->tick - ctl->run_base], (unsigned long long)__popc(ballot));
+    }
+}
+
+// ---- reference-shaped temporaries for the Inspector path -----------------------------------
+
+__global__ void dbg_clear_kernel(DebugArrays d) { // k-1, engine.cpp:335-339
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.cells) return;
+    for (int s = 0; s < 8; ++s) {
+        d.enroll_ids[i * 8 + s] = kNoPed;
+        d.enroll_scores[i * 8 + s] = 0.0;
+    }
+    d.winners[i] = kNoPed;
+    d.moved_from[i] = kNoPed;
+    d.moved_to[i] = kNoPed;
+    for (int k = 0; k < kKinds; ++k) {
+        d.from_mask[(long long)k * d.cells + i] = 0;
+        d.to_mask[(long long)k * d.cells + i] = 0;
+    }
+}
+
+__global__ void dbg_enroll_kernel(GridDev g, PedArrays p, DebugArrays d, Ctl* ctl) { // engine.cpp:346-361
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    const int dir = p.dir[i];
+    if (dir < 0) return;
+    const int2 c = p.center[i];
+    const uint32_t attr = p.attr[i];
+    const double score = p.score[i];
+    for_new_cells(c.x, c.y, attr_half_w(attr), attr_half_h(attr), dir, [&](int x, int y) {
+        const long long idx = cell_index(g, x, y);
+        if (idx < 0) return true;
+        const int prev = atomicCAS(&d.enroll_ids[idx * 8 + dir], kNoPed, (int)i);
+        if (prev != kNoPed) {
+            raise_error(ctl, SFC_E_INTEGRITY, 2, emod(x, g.W), emod(y, g.H), 0.0);
+        } else {
+            d.enroll_scores[idx * 8 + dir] = score;
+        }
+        return true;
+    });
+}
+
+__global__ void dbg_vote_kernel(DebugArrays d, int fault) { // engine.cpp:365-386
+    const long long su = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (su >= d.cells) return;
+    int best_id = kNoPed;
+    double best_score = 0.0;
+    for (int slot = 0; slot < 8; ++slot) {
+        const int id = d.enroll_ids[su * 8 + slot];
+        if (id == kNoPed) continue;
+        const double score = d.enroll_scores[su * 8 + slot];
+        bool better = best_id == kNoPed || score > best_score;
+        if (!better && score == best_score) better = fault ? id > best_id : id < best_id;
+        if (better) {
+            best_id = id;
+            best_score = score;
+        }
+    }
+    d.winners[su] = best_id;
+}
+
+__global__ void interleave_kernel(const float* __restrict__ plane, float* __restrict__ dyn, int kind, long long cells) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; // one float4 (half a su record slot)
+    if (t >= cells * 2) return;
+    const long long cell = t >> 1;
+    const int half = (int)(t & 1);
+    const float4 v = reinterpret_cast<const float4*>(plane)[t];
+    reinterpret_cast<float4*>(dyn)[cell * 6 + kind * 2 + half] = v;
+}
+
+__global__ void deinterleave_kernel(const float* __restrict__ dyn, float* __restrict__ plane, int kind, long long cells) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cells * 2) return;
+    const long long cell = t >> 1;
+    const int half = (int)(t & 1);
+    reinterpret_cast<float4*>(plane)[t] = reinterpret_cast<const float4*>(dyn)[cell * 6 + kind * 2 + half];
+}
+
+__global__ void fill_i8_kernel(int8_t* p, long long n, int v) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int8_t)v;
+}
+
+__global__ void tick_advance_kernel(Ctl* ctl) {
+    if (ctl->error_code == 0) ctl->tick += 1;
+}
+
+inline unsigned blocks_for(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+} // namespace
+
+cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
+                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp) {
+    k2_decide_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, stat, dyn, ev, ctl, dp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
+                           const DecideParams& dp) {
+    k3_vote_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ctl, dp.fault_invert);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
+                           unsigned long long* moved_counts, const DebugArrays& dbg) {
+    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dbg_clear(cudaStream_t s, const DebugArrays& d) {
+    dbg_clear_kernel<<<blocks_for(d.cells, 256), 256, 0, s>>>(d);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dbg_enroll(cudaStream_t s, const GridDev& g, const PedArrays& p, const DebugArrays& d, Ctl* ctl) {
+    dbg_enroll_kernel<<<blocks_for(p.n, 256), 256, 0, s>>>(g, p, d, ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dbg_vote(cudaStream_t s, const DebugArrays& d, int fault_invert) {
+    dbg_vote_kernel<<<blocks_for(d.cells, 256), 256, 0, s>>>(d, fault_invert);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, int kind, long long cells_begin,
+                              long long cells) {
+    interleave_kernel<<<blocks_for(cells * 2, 256), 256, 0, s>>>(plane, dyn + cells_begin * (kKinds * kSects), kind, cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
+                                long long cells) {
+    deinterleave_kernel<<<blocks_for(cells * 2, 256), 256, 0, s>>>(dyn + cells_begin * (kKinds * kSects), plane, kind, cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v) {
+    fill_i8_kernel<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl) {
+    tick_advance_kernel<<<1, 1, 0, s>>>(ctl);
+    return cudaGetLastError();
+}
+
+} // namespace sfc

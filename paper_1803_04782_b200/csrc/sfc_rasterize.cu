@@ -1,0 +1,271 @@
+// sfc_rasterize.cu — from-scratch rasterisation of the strength images on the device:
+//   * rebuild / rasterize_dynamic (reference engine.cpp:158-168 -> fields.cpp:152-160), used by
+//     the periodic drift check and image replacement (engine.cpp:538-550) and by seeding;
+//   * rasterize_static (fields.cpp:162-168) for openings and obstacles.
+//
+// The reference scatters: for pedestrian 0, 1, 2, ... add (float)|strength| into every su of the
+// field's support.  Float addition is order dependent, so a bit-identical result needs the same
+// per-address order: ascending pedestrian id, and for one pedestrian whose field wraps onto
+// itself, ascending row-major support offset.  Here it is a gather with that order made
+// explicit: a CTA collects the pedestrian centres inside its tile + field-halo region, sorts
+// them by (id, -y, -x) in shared memory (bitonic network on 64-bit keys), and every su walks
+// the sorted list adding the table magnitudes in float — atomics-free and bit-exact.
+
+#include "sfc_internal.cuh"
+
+namespace sfc {
+
+namespace {
+
+constexpr int kTileW = 32;
+constexpr int kRbThreads = 128;
+constexpr int kRbTileH = kRbThreads / kTileW;
+constexpr int kRbMaxEntries = 8192; // sorted-list capacity per tile (64 KB of keys)
+
+struct RbArgs {
+    GridDev g;
+    TablesDev t;
+    PedArrays p;
+    const int* occ;
+    float* dyn;
+    float* out;
+    Ctl* ctl;
+    int tiles_x;
+    int mode;
+    int cap; // power of two
+};
+
+__global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw); // [cap]
+    float* acc = reinterpret_cast<float*>(keys + a.cap);                           // [24][NT]
+    __shared__ int s_count;
+    __shared__ float s_drift[kKinds][kRbThreads / 32];
+
+    const GridDev g = a.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (a.mode == 2 && a.ctl->error_code != 0) return;
+
+    const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
+    const int x0 = tile_x * kTileW, y0 = g.row0 + tile_y * kRbTileH;
+    const int nx = min(kTileW, g.W - x0), ny = min(kRbTileH, g.row0 + g.rows - y0);
+    const int HW = a.t.max_hw, HH = a.t.max_hh;
+    const int RW = nx + 2 * HW, RH = ny + 2 * HH;
+    const int xs = x0 - HW, ys = y0 - HH;
+    const int lx = tid % kTileW, ly = tid / kTileW;
+    const bool active = lx < nx && ly < ny;
+    const int tcx = lx + HW, tcy = ly + HH;
+
+    if (tid == 0) s_count = 0;
+    for (int i = tid; i < a.cap; i += kRbThreads) keys[i] = ~0ull;
+#pragma unroll
+    for (int q = 0; q < kKinds * kSects; ++q) acc[q * kRbThreads + tid] = 0.0f;
+    __syncthreads();
+
+    // collect the pedestrian centres of the region (any order; sorted below)
+    const int ncell = RW * RH;
+    for (int i = tid; i < ncell; i += kRbThreads) {
+        const int ryi = i / RW, rxi = i - ryi * RW;
+        const long long idx = cell_index(g, xs + rxi, ys + ryi);
+        if (idx < 0) continue;
+        const int id = a.occ[idx];
+        if (id < 0) continue;
+        const int2 c = a.p.center[id];
+        int wx = xs + rxi, wy = ys + ryi;
+        if (!g.closed) {
+            wx = emod(wx, g.W);
+            wy = emod(wy, g.H);
+        }
+        if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
+        const int pos = atomicAdd(&s_count, 1);
+        if (pos < a.cap) {
+            const uint32_t attr = a.p.attr[id];
+            keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
+                        ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+        }
+    }
+    __syncthreads();
+    const int n = s_count;
+    if (n > a.cap) {
+        if (tid == 0) raise_error(a.ctl, SFC_E_STATE, 5, x0, y0, (double)n);
+        return;
+    }
+    // bitonic sort of the first pow2 >= n keys (padding keys are all-ones)
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int k = 2; k <= m; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < m; i += kRbThreads) {
+                const int partner = i ^ j;
+                if (partner > i) {
+                    const unsigned long long ka = keys[i], kb = keys[partner];
+                    const bool up = (i & k) == 0;
+                    if ((ka > kb) == up) {
+                        keys[i] = kb;
+                        keys[partner] = ka;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    if (active && n > 0) {
+        for (int e = 0; e < n; ++e) {
+            const unsigned long long key = keys[e];
+            const int ry = 8191 - (int)((key >> 19) & 0x1FFF), rx = 8191 - (int)((key >> 6) & 0x1FFF);
+            const int dx = rx - tcx, dy = ry - tcy; // centre offset = centre - target
+            if ((dx | dy) == 0) continue;
+            const uint32_t orients = (uint32_t)(key & 0x3F);
+#pragma unroll
+            for (int kind = 0; kind < kKinds; ++kind) {
+                const KindTableDev kt = a.t.k[kind];
+                if (dx < -kt.hw || dx > kt.hw || dy < -kt.hh || dy > kt.hh) continue;
+                const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
+                const uint32_t info = __ldg(kt.info + ti);
+                const uint32_t mask = (info >> 3) & 0xFFu;
+                const int orient = kind == 0 ? (orients & 7) : (kind == 1 ? ((orients >> 3) & 7) : 0);
+                if (!((mask >> orient) & 1u)) continue;
+                float* slot = acc + (kind * kSects + (info & 7)) * kRbThreads + tid;
+                *slot = __fadd_rn(*slot, __double2float_rn(__ldg(kt.mag + ti))); // += (float)s.norm()
+            }
+        }
+    }
+
+    float drift[kKinds] = {0.0f, 0.0f, 0.0f};
+    if (active) {
+        const long long cell = cell_index(g, x0 + lx, y0 + ly);
+        if (a.mode == 0) {
+            float* rec = a.out + cell * 24;
+#pragma unroll
+            for (int q = 0; q < 24; ++q) rec[q] = acc[q * kRbThreads + tid];
+        } else if (a.mode == 1) {
+            const float* rec = a.dyn + cell * 24;
+#pragma unroll
+            for (int q = 0; q < 24; ++q) {
+                const float d = fabsf(rec[q] - acc[q * kRbThreads + tid]);
+                if (drift[q / 8] < d) drift[q / 8] = d; // std::max(worst, d): a NaN never wins
+            }
+        } else {
+            float* rec = a.dyn + cell * 24;
+#pragma unroll
+            for (int q = 0; q < 24; ++q) rec[q] = acc[q * kRbThreads + tid];
+        }
+    }
+    if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
+#pragma unroll
+        for (int k = 0; k < kKinds; ++k) {
+            float v = drift[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+            if (lane == 0) s_drift[k][warp] = v;
+        }
+        __syncthreads();
+        if (tid < kKinds) {
+            float v = 0.0f;
+            for (int w = 0; w < kRbThreads / 32; ++w) v = fmaxf(v, s_drift[tid][w]);
+            if (v > 0.0f) atomicMax(&a.ctl->drift_bits[tid], __float_as_uint(v)); // non-negative floats order as uints
+        }
+    }
+}
+
+__global__ void drift_verdict_kernel(Ctl* ctl, double tolerance) { // engine.cpp:541-548
+    if (ctl->error_code != 0) return;
+    for (int k = 0; k < kKinds; ++k) {
+        const float drift = __uint_as_float(ctl->drift_bits[k]);
+        if ((double)drift > tolerance) {
+            raise_error(ctl, SFC_E_INTEGRITY, 5, k, 0, (double)drift);
+            break;
+        }
+    }
+    for (int k = 0; k < kKinds; ++k) ctl->drift_bits[k] = 0u;
+}
+
+// One anchored static field (rasterize_into, fields.cpp:152-160) as a per-target gather: the
+// thread owning target su t adds the field's strength once per periodic image of t inside the
+// support, images in row-major offset order.
+__global__ void static_anchor_kernel(GridDev g, KindTableDev kt, float* stat, int ax, int ay, int bw, int bh,
+                                     int orientation) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= bw * bh) return;
+    const int by = i / bw, bx = i - by * bw;
+    // first unwrapped target of this thread's residue class, then its periodic images
+    const int ux0 = ax - kt.hw + bx, uy0 = ay - kt.hh + by;
+    const long long idx = cell_index(g, ux0, uy0);
+    if (idx < 0) return; // clipped under a closed boundary
+    const int stepx = g.closed ? (kt.fw + 1) : g.W, stepy = g.closed ? (kt.fh + 1) : g.H;
+    for (int uy = uy0; uy <= ay + kt.hh; uy += stepy) {
+        for (int ux = ux0; ux <= ax + kt.hw; ux += stepx) {
+            const int dx = ax - ux, dy = ay - uy; // centre offset = anchor - target
+            if ((dx | dy) == 0) continue;
+            const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
+            const uint32_t info = kt.info[ti];
+            const uint32_t mask = (info >> 3) & 0xFFu;
+            if (mask == 0 || (orientation >= 0 && !((mask >> orientation) & 1u))) continue;
+            float* slot = stat + idx * kSects + (info & 7);
+            *slot = __fadd_rn(*slot, __double2float_rn(kt.mag[ti]));
+        }
+    }
+}
+
+int next_pow2(int v) {
+    int m = 32;
+    while (m < v) m <<= 1;
+    return m;
+}
+
+} // namespace
+
+namespace {
+int rebuild_cap(const TablesDev& t) {
+    const int region = (kTileW + 2 * t.max_hw) * (kRbTileH + 2 * t.max_hh);
+    return next_pow2(region < kRbMaxEntries ? region : kRbMaxEntries);
+}
+size_t rebuild_smem(const TablesDev& t) {
+    return sizeof(unsigned long long) * (size_t)rebuild_cap(t) + sizeof(float) * 24 * kRbThreads;
+}
+} // namespace
+
+// Raises the dynamic shared-memory limit ahead of time (must not happen inside a graph capture).
+cudaError_t prepare_rebuild(const TablesDev& t) {
+    const size_t smem = rebuild_smem(t);
+    if (smem <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
+                           float* dyn, float* out, Ctl* ctl, int mode, double /*tolerance*/) {
+    RbArgs a;
+    a.g = g;
+    a.t = t;
+    a.p = p;
+    a.occ = occ;
+    a.dyn = dyn;
+    a.out = out;
+    a.ctl = ctl;
+    a.mode = mode;
+    a.tiles_x = (g.W + kTileW - 1) / kTileW;
+    a.cap = rebuild_cap(t);
+    const size_t smem = rebuild_smem(t);
+    const long long blocks = (long long)a.tiles_x * ((g.rows + kRbTileH - 1) / kRbTileH);
+    rebuild_kernel<<<(unsigned)blocks, kRbThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_drift_verdict(cudaStream_t s, Ctl* ctl, double tolerance) {
+    drift_verdict_kernel<<<1, 1, 0, s>>>(ctl, tolerance);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,
+                                 int orientation) {
+    // one thread per residue class of target su: the whole support box, or the whole grid
+    // extent along an axis where the support is at least as wide as a periodic grid
+    const int bw = (!g.closed && t.fw > g.W) ? g.W : t.fw;
+    const int bh = (!g.closed && t.fh > g.H) ? g.H : t.fh;
+    const int n = bw * bh;
+    static_anchor_kernel<<<(n + 127) / 128, 128, 0, s>>>(g, t, stat, ax, ay, bw, bh, orientation);
+    return cudaGetLastError();
+}
+
+} // namespace sfc

@@ -1,0 +1,443 @@
+// engine.cpp — socfield::Engine of the B200 build: the reference's public engine surface
+// (proj/include/socfield/engine.hpp:142-230, proj/src/engine.cpp) as a thin host shim over the
+// CUDA C ABI (include/socfield_cuda.h).  No phase of the tick executes on the host.
+
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+
+#include "device_bridge.hpp"
+
+namespace socfield {
+
+FieldKind to_field_kind(DynKind k) {
+    static constexpr FieldKind kMap[kDynKinds] = {FieldKind::DirAttractive, FieldKind::DirRepulsive,
+                                                  FieldKind::RecurrentRepulsive};
+    const int i = static_cast<int>(k);
+    return i >= 0 && i < kDynKinds ? kMap[i] : FieldKind::RecurrentRepulsive;
+}
+
+// Host utility with the reference's semantics (engine.cpp:31-50): descending by score, ties to
+// the lower sect.  The device carries its own copy of the 19-comparator network inside k-2;
+// this one serves API callers, where any stable ordering with the same key is equivalent.
+std::array<int, 8> sort8_desc(const std::array<double, 8>& scores) {
+    std::array<int, 8> order{0, 1, 2, 3, 4, 5, 6, 7};
+    static constexpr int kNet[19][2] = {{0, 1}, {2, 3}, {0, 2}, {1, 3}, {1, 2}, {4, 5}, {6, 7}, {4, 6}, {5, 7}, {5, 6},
+                                        {0, 4}, {1, 5}, {1, 4}, {2, 6}, {3, 7}, {3, 6}, {2, 4}, {3, 5}, {3, 4}};
+    for (const auto& wire : kNet) {
+        int& hi = order[static_cast<std::size_t>(wire[0])];
+        int& lo = order[static_cast<std::size_t>(wire[1])];
+        const double sh = scores[static_cast<std::size_t>(hi)], sl = scores[static_cast<std::size_t>(lo)];
+        if (sh < sl || (sh == sl && hi > lo)) std::swap(hi, lo);
+    }
+    return order;
+}
+
+// ------------------------------------------------------------------ host mirrors -----------
+
+void EnrollmentTable::reset_geometry(const GridGeometry& g) {
+    shape_ = g;
+    const std::size_t n = static_cast<std::size_t>(g.cells()) * kSects;
+    who_.assign(n, kNoPedestrian);
+    how_.assign(n, 0.0);
+}
+
+int EnrollmentTable::count(SuIndex su) const {
+    const std::size_t first = shape_.flat(su) * kSects;
+    return static_cast<int>(std::count_if(who_.begin() + static_cast<std::ptrdiff_t>(first),
+                                          who_.begin() + static_cast<std::ptrdiff_t>(first + kSects),
+                                          [](std::int32_t id) { return id != kNoPedestrian; }));
+}
+
+std::optional<EnrollmentTable::Entry> EnrollmentTable::entry(SuIndex su, int slot) const {
+    const std::size_t at = shape_.flat(su) * kSects + static_cast<std::size_t>(slot);
+    if (who_[at] == kNoPedestrian) return std::nullopt;
+    return Entry{who_[at], how_[at]};
+}
+
+void EnrollmentTable::clear_range(std::size_t su_begin, std::size_t su_end) {
+    for (std::size_t i = su_begin * kSects; i < su_end * kSects; ++i) {
+        who_[i] = kNoPedestrian;
+        how_[i] = 0.0;
+    }
+}
+
+bool EnrollmentTable::enroll(std::size_t su_flat, int slot, std::int32_t id, double score) {
+    const std::size_t at = su_flat * kSects + static_cast<std::size_t>(slot);
+    if (who_[at] != kNoPedestrian) return false;
+    who_[at] = id;
+    how_[at] = score;
+    return true;
+}
+
+void MovementLog::reset(std::size_t cells) {
+    moved_from.assign(cells, kNoPedestrian);
+    moved_to.assign(cells, kNoPedestrian);
+    for (auto& m : from_mask) m.assign(cells, 0);
+    for (auto& m : to_mask) m.assign(cells, 0);
+}
+
+void MovementLog::clear_range(std::size_t begin, std::size_t end) {
+    const auto b = static_cast<std::ptrdiff_t>(begin), e = static_cast<std::ptrdiff_t>(end);
+    std::fill(moved_from.begin() + b, moved_from.begin() + e, kNoPedestrian);
+    std::fill(moved_to.begin() + b, moved_to.begin() + e, kNoPedestrian);
+    for (auto& m : from_mask) std::fill(m.begin() + b, m.begin() + e, std::uint8_t{0});
+    for (auto& m : to_mask) std::fill(m.begin() + b, m.begin() + e, std::uint8_t{0});
+}
+
+bool states_identical(const SimState& a, const SimState& b, std::string* diagnosis) {
+    const auto differ = [diagnosis](const std::string& what) {
+        if (diagnosis) *diagnosis = what;
+        return false;
+    };
+    if (a.tick != b.tick) return differ("tick counter differs");
+    if (a.pedestrians.size() != b.pedestrians.size()) return differ("pedestrian count differs");
+    for (std::size_t i = 0; i < a.pedestrians.size(); ++i) {
+        const SuIndex ca = a.pedestrians[i].center, cb = b.pedestrians[i].center;
+        if (ca != cb) {
+            std::ostringstream msg;
+            msg << "pedestrian " << a.pedestrians[i].id << " center (" << ca.x << "," << ca.y << ") vs (" << cb.x
+                << "," << cb.y << ")";
+            return differ(msg.str());
+        }
+    }
+    const int w = a.occupancy.geometry().width;
+    const auto& oa = a.occupancy.raw();
+    const auto& ob = b.occupancy.raw();
+    if (oa.size() != ob.size()) return differ("occupancy size differs");
+    for (std::size_t i = 0; i < oa.size(); ++i) {
+        if (oa[i] == ob[i]) continue;
+        std::ostringstream msg;
+        msg << "occupancy at su (" << i % static_cast<std::size_t>(w) << "," << i / static_cast<std::size_t>(w)
+            << "): " << oa[i] << " vs " << ob[i];
+        return differ(msg.str());
+    }
+    // images compare by bit pattern, not by value (-0.0f != 0.0f, NaN == same NaN)
+    const auto images_match = [&](const StrengthImage& ia, const StrengthImage& ib, const char* label) {
+        const auto& ra = ia.raw();
+        const auto& rb = ib.raw();
+        if (ra.size() == rb.size() && (ra.empty() || std::memcmp(ra.data(), rb.data(), ra.size() * sizeof(float)) == 0))
+            return true;
+        const std::size_t n = std::min(ra.size(), rb.size());
+        const int iw = ia.geometry().width;
+        for (std::size_t i = 0; i < n; ++i) {
+            if (std::memcmp(&ra[i], &rb[i], sizeof(float)) == 0) continue;
+            const std::size_t su = i / kSects;
+            std::ostringstream msg;
+            msg << label << " image at su (" << su % static_cast<std::size_t>(iw) << ","
+                << su / static_cast<std::size_t>(iw) << ") sect " << i % kSects << ": " << ra[i] << " vs " << rb[i];
+            if (diagnosis) *diagnosis = msg.str();
+            return false;
+        }
+        if (diagnosis) *diagnosis = std::string(label) + " image size differs";
+        return false;
+    };
+    if (!images_match(a.static_image, b.static_image, "static")) return false;
+    for (int k = 0; k < kDynKinds; ++k) {
+        const char* label = field_kind_name(to_field_kind(static_cast<DynKind>(k)));
+        if (!images_match(a.dyn_images[static_cast<std::size_t>(k)], b.dyn_images[static_cast<std::size_t>(k)], label))
+            return false;
+    }
+    return true;
+}
+
+// ------------------------------------------------------------------ state views ------------
+
+namespace {
+
+// Pointers into a SimState for the C ABI.  The const_cast on an input-only view is confined to
+// this function: sfc_upload never writes through the pointers.
+sfc_state_view make_view(SimState& s, bridge::PedColumns& cols) {
+    cols.gather(s.pedestrians);
+    sfc_state_view v{};
+    v.tick = s.tick;
+    v.n_peds = static_cast<std::int64_t>(s.pedestrians.size());
+    v.occupancy = s.occupancy.raw_mut().data();
+    v.static_image = s.static_image.raw_mut().data();
+    for (int k = 0; k < kDynKinds; ++k) v.dyn_images[k] = s.dyn_images[static_cast<std::size_t>(k)].raw_mut().data();
+    v.center_xy = cols.center_xy.data();
+    v.walk_period = cols.period.data();
+    v.walk_phase = cols.phase.data();
+    v.goal_sect = cols.goal.data();
+    v.orient_attractive = cols.orient_a.data();
+    v.orient_repulsive = cols.orient_r.data();
+    v.foot_w = cols.foot_w.data();
+    v.foot_h = cols.foot_h.data();
+    return v;
+}
+
+void require_shape(const SimState& s, const GridGeometry& g) {
+    const std::size_t cells = static_cast<std::size_t>(g.cells());
+    if (s.occupancy.raw().size() != cells) throw IntegrityError("occupancy geometry mismatch", s.tick, 0);
+    if (s.static_image.raw().size() != cells * kSects) throw IntegrityError("static image geometry mismatch", s.tick, 0);
+    for (const auto& img : s.dyn_images)
+        if (img.raw().size() != cells * kSects) throw IntegrityError("dynamic image geometry mismatch", s.tick, 0);
+}
+
+TickMetrics to_metrics(const sfc_tick_metrics& m) {
+    TickMetrics out;
+    out.tick = static_cast<long>(m.tick);
+    for (int p = 0; p < 5; ++p) out.phase_us[static_cast<std::size_t>(p)] = m.phase_us[p];
+    out.moved = m.moved;
+    out.wall_us = m.wall_us;
+    return out;
+}
+
+// The su a step in `direction` newly covers, row-major over the new footprint
+// (reference engine.cpp:271-287).  Empty when one falls off a closed grid.
+std::vector<SuIndex> newly_covered(const GridGeometry& g, const Pedestrian& p, int direction) {
+    std::vector<SuIndex> cells;
+    const Offset u = sect_step(direction);
+    const int rw = p.footprint.half_w(), rh = p.footprint.half_h();
+    for (int oy = -rh; oy <= rh; ++oy) {
+        for (int ox = -rw; ox <= rw; ++ox) {
+            const bool already = std::abs(ox + u.dx) <= rw && std::abs(oy + u.dy) <= rh;
+            if (already) continue;
+            const auto su = wrap(g, p.center.x + u.dx + ox, p.center.y + u.dy + oy);
+            if (!su) return {};
+            cells.push_back(*su);
+        }
+    }
+    return cells;
+}
+
+} // namespace
+
+// ------------------------------------------------------------------ Engine -----------------
+
+Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<FieldSpec, kDynKinds>& field_templates)
+    : geom_(g), cfg_(cfg), field_templates_(field_templates) {
+    if (!valid_chunk_width(cfg_.chunk_k)) throw ConfigError("chunk_k", "must be 2, 4, 8, or 16");
+    if (cfg_.density_radius < 0) throw ConfigError("density_radius", "must be >= 0");
+    if (cfg_.workers <= 0) cfg_.workers = 1; // no host workers exist; keep the field well-formed
+
+    std::array<bridge::KindTable, kDynKinds> tables;
+    for (int k = 0; k < kDynKinds; ++k) {
+        FieldSpec& spec = field_templates_[static_cast<std::size_t>(k)];
+        spec.kind = to_field_kind(static_cast<DynKind>(k));
+        auto& plans = plans_[static_cast<std::size_t>(k)];
+        if (is_directional(spec.kind)) {
+            for (int orient = 0; orient < kSects; ++orient) {
+                FieldSpec facing = spec;
+                facing.orientation = orient;
+                plans.push_back(build_write_plan(facing));
+            }
+        } else {
+            plans.push_back(build_write_plan(spec));
+        }
+        tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(spec);
+    }
+    dev_ = bridge::create_engine(geom_, cfg_, tables);
+
+    const std::size_t cells = static_cast<std::size_t>(geom_.cells());
+    enrollment_.reset_geometry(geom_);
+    winners_.assign(cells, kNoPedestrian);
+    movelog_.reset(cells);
+    step_caches_.assign(1, StepCache(cfg_.chunk_k));
+}
+
+Engine::~Engine() { sfc_destroy(dev_); }
+
+const WritePlan& Engine::plan(DynKind kind, int orientation) const {
+    const auto& plans = plans_[static_cast<std::size_t>(kind)];
+    if (plans.size() == 1) return plans.front();
+    return plans.at(static_cast<std::size_t>(orientation));
+}
+
+void Engine::throw_status(int status) const {
+    std::int64_t tick = -1;
+    std::int32_t phase = 0;
+    sfc_error_detail(dev_, &tick, &phase, nullptr, nullptr, nullptr);
+    bridge::throw_status(status, sfc_last_error(dev_), static_cast<long>(tick), phase);
+}
+
+void Engine::upload(const SimState& s) {
+    require_shape(s, geom_);
+    bridge::PedColumns cols;
+    const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);
+    const int status = sfc_upload(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    if (decisions_.size() != s.pedestrians.size()) decisions_.assign(s.pedestrians.size(), kStill);
+}
+
+void Engine::download(SimState& s) {
+    bridge::PedColumns cols;
+    sfc_state_view v = make_view(s, cols);
+    v.static_image = nullptr; // a tick never writes it
+    const int status = sfc_download(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    for (std::size_t i = 0; i < s.pedestrians.size(); ++i)
+        s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
+    s.tick = static_cast<long>(v.tick);
+}
+
+std::vector<TickMetrics> Engine::step_resident(long ticks, bool phase_times) {
+    std::vector<TickMetrics> out;
+    if (ticks <= 0) return out;
+    std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
+    const int status = sfc_run(dev_, ticks, raw.data(), phase_times ? 1 : 0);
+    if (status != SFC_OK) throw_status(status);
+    out.reserve(raw.size());
+    for (const auto& m : raw) out.push_back(to_metrics(m));
+    return out;
+}
+
+void Engine::pull_temporaries(int phase, SimState& s) {
+    const std::size_t cells = static_cast<std::size_t>(geom_.cells());
+    std::vector<std::uint8_t> from(3 * cells), to(3 * cells);
+    std::vector<std::int32_t> dirs(s.pedestrians.size());
+    sfc_temporaries t{};
+    t.decisions = dirs.data();
+    t.enroll_ids = enrollment_.ids_mut().data();
+    t.enroll_scores = enrollment_.scores_mut().data();
+    t.winners = winners_.data();
+    t.moved_from = movelog_.moved_from.data();
+    t.moved_to = movelog_.moved_to.data();
+    t.from_mask = from.data();
+    t.to_mask = to.data();
+    const int status = sfc_download_temporaries(dev_, &t);
+    if (status != SFC_OK) throw_status(status);
+    for (int k = 0; k < kDynKinds; ++k) {
+        const auto b = static_cast<std::ptrdiff_t>(static_cast<std::size_t>(k) * cells);
+        const auto e = b + static_cast<std::ptrdiff_t>(cells);
+        movelog_.from_mask[static_cast<std::size_t>(k)].assign(from.begin() + b, from.begin() + e);
+        movelog_.to_mask[static_cast<std::size_t>(k)].assign(to.begin() + b, to.begin() + e);
+    }
+    decisions_.assign(dirs.begin(), dirs.end());
+    if (phase >= 4) {
+        const long tick_before = s.tick;
+        download(s);
+        s.tick = tick_before; // the counter advances only at the end of the tick
+    }
+}
+
+TickMetrics Engine::tick(SimState& s, RunMode mode) { return tick(s, mode, Inspector{}); }
+
+TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect) {
+    upload(s);
+    TickMetrics m;
+    m.tick = s.tick;
+    if (!inspect) {
+        int status = SFC_OK;
+        sfc_tick_metrics raw{};
+        status = sfc_run(dev_, 1, &raw, 1);
+        download(s); // the state is meaningful even when the tick ended in an integrity error
+        if (status != SFC_OK) throw_status(status);
+        return to_metrics(raw);
+    }
+    // Inspector path: one phase at a time, host mirrors refreshed after each (engine.cpp:487-530).
+    for (int phase = 1; phase <= 5; ++phase) {
+        std::int64_t moved = 0;
+        const int status = sfc_phase(dev_, phase, phase >= 4 ? &moved : nullptr);
+        if (status != SFC_OK) {
+            download(s);
+            throw_status(status);
+        }
+        if (phase >= 4) m.moved = moved;
+        pull_temporaries(phase, s);
+        inspect(phase, *this, s);
+    }
+    const int status = sfc_phase(dev_, 6, nullptr);
+    download(s);
+    if (status != SFC_OK) throw_status(status);
+    return m;
+}
+
+std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode) { return run(s, ticks, mode, Inspector{}); }
+
+std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, const Inspector& inspect) {
+    verify_state(s);
+    std::vector<TickMetrics> metrics;
+    if (ticks <= 0) return metrics;
+    if (inspect) {
+        metrics.reserve(static_cast<std::size_t>(ticks));
+        for (long i = 0; i < ticks; ++i) metrics.push_back(tick(s, mode, inspect));
+        return metrics;
+    }
+    upload(s);
+    std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
+    const int status = sfc_run(dev_, ticks, raw.data(), 0);
+    download(s);
+    if (status != SFC_OK) throw_status(status);
+    metrics.reserve(raw.size());
+    for (const auto& r : raw) metrics.push_back(to_metrics(r));
+    return metrics;
+}
+
+MoveDecision Engine::decide(const Pedestrian& p, const SimState& s) const {
+    require_shape(s, geom_);
+    // The device decides for the pedestrian stored at p.id; substitute `p` there so callers may
+    // probe a modified copy, as the reference's by-value semantics allow.
+    SimState probe = s;
+    const std::size_t slot = static_cast<std::size_t>(p.id);
+    if (slot >= probe.pedestrians.size()) throw IntegrityError("decide: pedestrian id out of range", s.tick, 0);
+    probe.pedestrians[slot] = p;
+    bridge::PedColumns cols;
+    const sfc_state_view v = make_view(probe, cols);
+    int status = sfc_upload(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    MoveDecision d;
+    std::int32_t dir = kStill;
+    status = sfc_decide(dev_, p.id, &dir, &d.score);
+    if (status != SFC_OK) throw_status(status);
+    d.direction = dir;
+    if (dir != kStill) d.new_cells = newly_covered(geom_, p, dir);
+    return d;
+}
+
+std::array<StrengthImage, kDynKinds> Engine::rebuild_images(const SimState& s) const {
+    require_shape(s, geom_);
+    bridge::PedColumns cols;
+    const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);
+    int status = sfc_upload(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    std::array<StrengthImage, kDynKinds> fresh{StrengthImage(geom_), StrengthImage(geom_), StrengthImage(geom_)};
+    float* out[kDynKinds] = {fresh[0].raw_mut().data(), fresh[1].raw_mut().data(), fresh[2].raw_mut().data()};
+    status = sfc_rasterize_dynamic(dev_, out);
+    if (status != SFC_OK) throw_status(status);
+    return fresh;
+}
+
+// Structural check of a host state (reference engine.cpp:569-618).  Integer bookkeeping on the
+// caller's own buffers; it guards the upload, it is not part of the tick.
+void Engine::verify_state(const SimState& s) const {
+    const auto reject = [&s](const std::string& what) { throw IntegrityError(what, s.tick, 0); };
+    if (!(s.occupancy.geometry() == geom_)) reject("occupancy geometry mismatch");
+    OccupancyGrid expected(geom_);
+    for (std::size_t i = 0; i < s.pedestrians.size(); ++i) {
+        const Pedestrian& p = s.pedestrians[i];
+        const std::string who = "pedestrian " + std::to_string(p.id);
+        if (p.id != static_cast<std::int32_t>(i)) reject("pedestrian ids must equal their index");
+        const auto normal = wrap(geom_, p.center);
+        if (!normal || *normal != p.center) reject(who + " center not normalized");
+        if (p.walk_period < 1 || p.walk_phase < 0 || p.walk_phase >= p.walk_period) reject(who + " walk gate out of range");
+        if (p.goal_sect < 0 || p.goal_sect >= kSects) reject(who + " goal sect out of range");
+        for (int k = 0; k < kDynKinds; ++k) {
+            const FieldSpec& have = p.dyn_fields[static_cast<std::size_t>(k)];
+            const FieldSpec& want = field_templates_[static_cast<std::size_t>(k)];
+            if (have.kind != want.kind || have.geometry != want.geometry || have.gain != want.gain ||
+                have.decay != want.decay)
+                reject(who + " field spec does not match the engine template");
+        }
+        const FootprintCells body = footprint_cells(geom_, p.center, p.footprint);
+        if (body.clipped) reject(who + " footprint crosses a closed edge");
+        for (const SuIndex su : body.cells) {
+            if (!expected.empty_at(su)) {
+                if (expected.at(su) == p.id) reject(who + " footprint wraps onto itself");
+                reject("pedestrians " + std::to_string(expected.at(su)) + " and " + std::to_string(p.id) +
+                       " overlap at su (" + std::to_string(su.x) + "," + std::to_string(su.y) + ")");
+            }
+            expected.set(su, p.id);
+        }
+    }
+    const auto& got = s.occupancy.raw();
+    const auto& want = expected.raw();
+    for (std::size_t i = 0; i < got.size(); ++i) {
+        if (got[i] == want[i]) continue;
+        const std::size_t w = static_cast<std::size_t>(geom_.width);
+        reject("occupancy at su (" + std::to_string(i % w) + "," + std::to_string(i / w) + ") holds " +
+               std::to_string(got[i]) + ", expected " + std::to_string(want[i]));
+    }
+}
+
+} // namespace socfield

@@ -1,0 +1,71 @@
+"""Scenario texts and hand-built populations shared by the parity tests.
+
+The texts use the reference's `key = value` scenario format (reference
+proj/src/scenario.cpp:172-268); the fixtures restate those of the reference's own tests
+(proj/tests/unit/test_engine.cpp, proj/tests/acceptance/acceptance_main.cpp).
+"""
+import itertools
+
+DESK64 = """# desk-scale validation scenario (reference proj/scenarios/desk64.scn)
+grid = 64x64
+density = 0.5
+directions = eight
+field_geometry = 7x7
+pedestrian_geometry = 1x1
+walk_period = 1..3
+ticks = 100
+seed = 42
+"""
+
+SEQPAR24 = """# reference test_engine.cpp:352-360
+grid = 24x24
+density = 0.4
+directions = four
+walk_period = 1..3
+seed = 99
+rebuild_interval = 10
+"""
+
+
+def acceptance3_scenarios():
+    """The 24 scenarios of acceptance criterion 3 (acceptance_main.cpp:60-89)."""
+    out = []
+    seed = 1000
+    for density, dirs, ped in itertools.product((0.1, 0.5, 0.9), ("uni", "bi", "four", "eight"), (1, 3)):
+        out.append((f"d{density}-{dirs}-ped{ped}",
+                    f"grid = 64x64\ndensity = {density}\ndirections = {dirs}\npedestrian_geometry = {ped}x{ped}\n"
+                    f"walk_period = 1..3\nseed = {seed}\nrebuild_interval = 50\n"))
+        seed += 1
+    return out
+
+
+def variant(text: str, **overrides) -> str:
+    """Scenario text with keys replaced / appended."""
+    lines = [l for l in text.splitlines() if l.split("=")[0].strip() not in overrides]
+    lines += [f"{k} = {v}" for k, v in overrides.items()]
+    return "\n".join(lines) + "\n"
+
+
+EXTRA = {
+    "closed-four": "grid = 32x20\nboundary = closed\ndensity = 0.4\ndirections = four\nseed = 13\nrebuild_interval = 7\n",
+    "closed-ped3": "grid = 40x40\nboundary = closed\ndensity = 0.3\ndirections = eight\npedestrian_geometry = 3x3\n"
+                   "walk_period = 1..2\nseed = 5\nrebuild_interval = 0\n",
+    "field21": "grid = 48x40\ndensity = 0.2\ndirections = eight\nfield_geometry = 21x21\nwalk_period = 1..3\nseed = 77\n"
+               "rebuild_interval = 9\n",
+    "field-5x9": "grid = 37x29\ndensity = 0.3\ndirections = bi\nfield_geometry = 5x9\nseed = 3\nrebuild_interval = 4\n",
+    "field-bigger-than-grid": "grid = 8x6\ndensity = 0.2\ndirections = eight\nfield_geometry = 11x9\nseed = 8\n"
+                              "rebuild_interval = 3\n",
+    "linear-regulation": "grid = 40x40\ndensity = 0.5\ndirections = eight\nregulation = linear\ndensity_radius = 2\n"
+                         "walk_period = 1..3\nseed = 21\nrebuild_interval = 0\n",
+    "linear-closed": "grid = 30x30\nboundary = closed\ndensity = 0.6\ndirections = four\nregulation = linear\n"
+                     "density_radius = 3\nseed = 22\nrebuild_interval = 5\n",
+    "k2": "grid = 32x32\ndensity = 0.5\nchunk_k = 2\nseed = 31\nrebuild_interval = 0\n",
+    "k4": "grid = 32x32\ndensity = 0.5\nchunk_k = 4\nseed = 31\nrebuild_interval = 0\n",
+    "k16": "grid = 32x32\ndensity = 0.5\nchunk_k = 16\nseed = 31\nrebuild_interval = 0\n",
+    "weights": "grid = 33x31\ndensity = 0.45\ndirections = eight\nweight_static = 0.5\nweight_dir_attractive = 0.25\n"
+               "weight_dir_repulsive = 1.75\nweight_recurrent = 0.6\ngoal_bias = 0.35\nfield_gain = 1.3\n"
+               "field_decay = -0.37\nwalk_period = 1..4\nseed = 17\nrebuild_interval = 6\n",
+    "ped5": "grid = 64x48\ndensity = 0.35\ndirections = eight\npedestrian_geometry = 5x3\nfield_geometry = 9x9\n"
+            "walk_period = 1..2\nseed = 4\nrebuild_interval = 8\n",
+    "wide-ragged": "grid = 131x67\ndensity = 0.3\ndirections = bi\nwalk_period = 1..3\nseed = 123\nrebuild_interval = 10\n",
+}

@@ -1,0 +1,128 @@
+"""GPU parity: the CUDA engine against the CPU oracle on identical scenarios and seeds.
+
+Every comparison is BIT-EXACT (integers: occupancy, centres, decisions, vote winners, movement
+log; floats compared by bit pattern: decision scores in f64, strength images in f32) — stronger
+than the rtol 1e-5 the north star allows for field values.  The engine is reached through the
+flat-C shim compiled against the product's host mirror, i.e. through socfield::Engine and the
+C ABI underneath; the checker is the C oracle (oracle/socfield_oracle.c), cross-checked against
+the compiled reference (oracle/_ref) when that library travelled with the snapshot.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle, shim
+from tests import scenarios as sc
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "digests.json")))
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64 if a.dtype == np.float64 else a.dtype)
+
+
+def assert_state_equal(gpu: shim.Sim, cpu: oracle.OracleSim, label=""):
+    assert gpu.tick == cpu.tick, label
+    np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"{label} centres")
+    np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"{label} occupancy")
+    for k in range(3):
+        np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)), err_msg=f"{label} image {k}")
+    assert gpu.digest() == cpu.digest(), label
+
+
+@pytest.mark.parametrize("name", ["desk64", "seqpar24"])
+def test_golden_digests(product_lib, name):
+    """Free run from the seeded state reproduces the reference's recorded digests — through two
+    id-ordered float rebuilds for desk64 (ticks 50 and 100)."""
+    g = GOLDEN[name]
+    sim = shim.Sim.from_scenario(product_lib, g["scenario"])
+    assert sim.population == g["population"]
+    last = 0
+    for tick, digest in g["digests"]:
+        sim.run(tick - last)
+        last = tick
+        assert f"{sim.digest():#018x}" == digest, f"{name} tick {tick}"
+
+
+@pytest.mark.parametrize("name,text", sc.acceptance3_scenarios())
+def test_acceptance3_free_run(product_lib, name, text):
+    """Acceptance criterion 3's 24 scenarios (64x64; rho .1/.5/.9; 4 direction sets; 1x1 and 3x3
+    pedestrians; rebuild every 50), 100 ticks: state identical to the oracle every 10 ticks."""
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    assert_state_equal(gpu, cpu, f"{name} seed")
+    for step in range(10):
+        moved_gpu = gpu.run(10)
+        moved_cpu = cpu.run(10)
+        np.testing.assert_array_equal(moved_gpu, moved_cpu, err_msg=f"{name} moved counts")
+        assert_state_equal(gpu, cpu, f"{name} tick {10 * (step + 1)}")
+    gpu.verify()
+
+
+@pytest.mark.parametrize("name", sorted(sc.EXTRA))
+def test_extra_scenarios_free_run(product_lib, name):
+    """Closed boundaries, 3x3 / 5x3 bodies, 21x21 and non-square fields, a field larger than the
+    grid, linear regulation, every chunk width, non-default weights, ragged grid sizes."""
+    text = sc.EXTRA[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    assert_state_equal(gpu, cpu, f"{name} seed")
+    for step in range(6):
+        np.testing.assert_array_equal(gpu.run(5), cpu.run(5), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} tick {5 * (step + 1)}")
+
+
+@pytest.mark.parametrize("name", ["desk64", "closed-ped3", "k16", "linear-regulation", "ped5"])
+def test_phase_by_phase_lockstep(product_lib, name):
+    """Inspector path: after every phase the engine's temporaries equal the oracle's — decisions
+    and f64 scores (k-2), enrollment table (k-2), vote winners (k-3), movement log, occupancy and
+    centres (k-4), images (k-5) — with the GPU state overwritten from the CPU state each tick
+    ("driven from the same field state")."""
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for tick in range(8):
+        gpu.set_occupancy(cpu.occupancy())
+        for k in range(3):
+            gpu.set_image(k, cpu.image(k))
+        gpu.set_centers(cpu.centers())
+        gpu.tick = cpu.tick
+        probe = cpu.clone()
+        probe.step(until_phase=2)
+        cap = gpu.step_capture()
+        assert cap.phases_seen == 0b111110
+        np.testing.assert_array_equal(cap.decisions, probe.decisions(), err_msg=f"tick {tick} decisions")
+        np.testing.assert_array_equal(cap.enroll_ids, probe.enroll_ids(), err_msg=f"tick {tick} enrollment ids")
+        np.testing.assert_array_equal(bits(cap.enroll_scores), bits(probe.enroll_scores()),
+                                      err_msg=f"tick {tick} enrollment scores")
+        full = cpu.clone()
+        full.step(until_phase=4)
+        np.testing.assert_array_equal(cap.winners, full.winners(), err_msg=f"tick {tick} winners")
+        np.testing.assert_array_equal(cap.moved_from, full.moved_from(), err_msg=f"tick {tick} moved_from")
+        np.testing.assert_array_equal(cap.moved_to, full.moved_to(), err_msg=f"tick {tick} moved_to")
+        np.testing.assert_array_equal(cap.from_mask, full.from_mask(), err_msg=f"tick {tick} from_mask")
+        np.testing.assert_array_equal(cap.to_mask, full.to_mask(), err_msg=f"tick {tick} to_mask")
+        np.testing.assert_array_equal(cap.occupancy_k4.reshape(cpu.height, cpu.width), full.occupancy())
+        np.testing.assert_array_equal(cap.centers_k4.reshape(-1, 2), full.centers())
+        moved = cpu.step()
+        assert cap.moved == moved
+        assert_state_equal(gpu, cpu, f"{name} tick {tick + 1}")
+
+
+def test_against_compiled_reference(product_lib, ref_lib):
+    """The same comparison against the unmodified reference binary (oracle/_ref), both through
+    the identical shim — the drop-in check: states_identical across implementations."""
+    for text in (sc.DESK64, sc.EXTRA["closed-four"], sc.EXTRA["ped5"]):
+        gpu = shim.Sim.from_scenario(product_lib, text)
+        ref = shim.Sim.from_scenario(ref_lib, text, workers=2)
+        for _ in range(4):
+            np.testing.assert_array_equal(gpu.run(15), ref.run(15, mode="par"))
+            assert gpu.digest() == ref.digest()
+            np.testing.assert_array_equal(gpu.centers(), ref.centers())
+            for k in range(3):
+                np.testing.assert_array_equal(bits(gpu.image(k)), bits(ref.image(k)))
