@@ -1,0 +1,25 @@
+"""Short device-resident run for ncu: seeds a bench workload, uploads it, steps a few ticks.
+
+    ncu ... python profiles/profile_target.py --workload c2 --ticks 8
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_1803_04782_b200 import socfield as sf  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2")
+ap.add_argument("--ticks", type=int, default=8)
+ap.add_argument("--warm", type=int, default=30)
+args = ap.parse_args()
+cfg, state = bench.build_state(sf, bench.WORKLOADS[args.workload])
+engine = sf.Engine(cfg)
+engine.upload(state)
+engine.step_resident(args.warm)      # let the crowd start moving (graph launches)
+m = engine.step_resident(args.ticks, True)  # plain launches, one kernel per phase
+print("moved per tick:", [x.moved for x in m])
