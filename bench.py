@@ -76,6 +76,7 @@ class ClockSampler(threading.Thread):
         self.index = index
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._halt = threading.Event()
+        self.recording = False  # NVML start-up happens before the timed region; samples only inside it
 
     def run(self):
         try:
@@ -91,12 +92,13 @@ class ClockSampler(threading.Thread):
                 nv.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap",
             }
             while not self._halt.is_set():
-                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                for bit, name in names.items():
-                    if mask & bit:
-                        self.reasons.add(name)
-                time.sleep(0.005)
+                if self.recording:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    for bit, name in names.items():
+                        if mask & bit:
+                            self.reasons.add(name)
+                time.sleep(0.002)
         except Exception as exc:  # NVML missing: record that, do not fail the bench
             self.reasons.add(f"nvml_unavailable:{type(exc).__name__}")
 
@@ -227,18 +229,20 @@ def main():
     assert P == w["peds"], (P, w["peds"])
 
     # ---- device-resident throughput ("value") ------------------------------------------------
+    sampler = ClockSampler(local)
+    sampler.start()
     engine.upload(state)
     for _ in range(warmup):
         engine.step_resident(TICKS_PER_STEP)
     c0 = engine.counters()
     barrier(dist, local)
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler.recording = True
     total_ms = 0.0
     for _ in range(args.steps):
         engine.step_resident(TICKS_PER_STEP)
         total_ms += engine.counters()["last_run_ms"]  # CUDA events on the engine's stream
     barrier(dist, local)
+    sampler.recording = False
     clocks = sampler.stop()
     c1 = engine.counters()
     total_ms = reduce_max(dist, local, total_ms)

@@ -36,7 +36,10 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "--fmad=false",  # decisions and field sums must not contract a*b+c
 ]
-CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off"]
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off", "-Wl,-Bsymbolic"]
+# One shared C++ runtime for every library in the process: this image's g++ wrapper finds only
+# the static libstdc++.a, and several private copies of it (one per .so) corrupt iostream state.
+STDCXX = ["-L/usr/lib/x86_64-linux-gnu", "-l:libstdc++.so.6"]
 
 
 def _newer(target: str, sources: list[str]) -> bool:
@@ -74,7 +77,7 @@ def build_host(force: bool = False, verbose: bool = True) -> str:
     sources = [os.path.join(HOST, s) for s in HOST_SOURCES]
     if force or _newer(target, sources + _headers() + [cuda]):
         _run([CXX, *CXX_FLAGS, "-I" + INCLUDE, "-I" + HOST, "-shared", "-o", target, *sources,
-              "-L" + LIB, "-lsocfield_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+              "-L" + LIB, "-lsocfield_cuda", *STDCXX, "-Wl,-rpath,$ORIGIN"], verbose)
     return target
 
 
@@ -86,7 +89,7 @@ def build_shim(force: bool = False, verbose: bool = True) -> str:
     if force or _newer(target, [src, hdr, host] + _headers()):
         _run([CXX, *CXX_FLAGS, "-Wno-comment", "-I" + INCLUDE, "-I" + os.path.join(ROOT, "oracle"),
               '-DSHIM_IMPL_NAME="b200-cuda"', "-shared", "-o", target, src,
-              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", *STDCXX, "-Wl,-rpath,$ORIGIN"], verbose)
     return target
 
 
@@ -102,7 +105,7 @@ def build_pybind(force: bool = False, verbose: bool = True) -> str:
     if force or _newer(target, [src, host] + _headers()):
         _run([CXX, *CXX_FLAGS, "-I" + INCLUDE, "-I" + HOST, "-I" + pybind11.get_include(),
               "-I" + sysconfig.get_paths()["include"], "-shared", "-o", target, src,
-              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", "-Wl,-rpath,$ORIGIN/../lib"], verbose)
+              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", *STDCXX, "-Wl,-rpath,$ORIGIN/../lib"], verbose)
     return target
 
 

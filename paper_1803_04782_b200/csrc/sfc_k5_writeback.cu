@@ -344,10 +344,16 @@ cudaError_t launch_variant(cudaStream_t stream, const K5Launch& l) {
     return cudaGetLastError();
 }
 
+// The attribute is per-function process state shared by every engine: only ever raise it.
 template <int K, int SG, int ROWS>
 cudaError_t prepare_variant(const TablesDev& t) {
-    return cudaFuncSetAttribute(k5_writeback_kernel<K, SG, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)k5_shape<K, SG, ROWS>(t).smem);
+    static size_t granted = 0;
+    const size_t want = k5_shape<K, SG, ROWS>(t).smem;
+    if (want <= granted) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(k5_writeback_kernel<K, SG, ROWS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (e == cudaSuccess) granted = want;
+    return e;
 }
 
 // Small fields (whole region staged at once): macro-tiles of 8 rows (two per warp).  Large fields: 4-row tiles
