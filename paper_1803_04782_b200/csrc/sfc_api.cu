@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -42,6 +43,7 @@ struct sfc_engine {
     cudaGraphExec_t graph = nullptr;
     bool graph_valid = false;
 
+    int k5_event_max = 64; // tuning knob, overridable with SFC_K5_EVENT_MAX (tests force either k-5 path)
     bool uploaded = false;
     long long tick = 0;
     sfc_counters counters{};
@@ -203,6 +205,7 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.ctl = e->ctl;
     l.chunk_k = e->cfg.chunk_k;
     l.advance_tick = advance;
+    l.ev_max = e->k5_event_max;
     return l;
 }
 
@@ -283,6 +286,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     };
     e->cfg = *cfg;
     e->device = cfg->device;
+    if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = std::atoi(knob);
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
     e->g.H = cfg->height;

@@ -160,6 +160,7 @@ struct K5Launch {
     Ctl* ctl;
     int chunk_k;
     int advance_tick; // fold "tick += 1" into the kernel (fast path)
+    int ev_max;       // k-5: event-count threshold between the scatter and the gather formulation
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp);

@@ -57,6 +57,8 @@ struct K5Args {
     int cap;       // cells staged per pass = event-list capacity
     int rw_max;    // region columns for a full tile
     int tab_smem;  // contributor tables fit in shared memory
+    int part_doubles; // size of the partial-sum / scatter region, in doubles
+    int ev_max;    // tiles with at most this many events in reach take the event-centric path
 };
 
 // K: StepCache width.  SG: sects accumulated per walk (SG * K <= 64: the dirty set is one 64-bit
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
 
     // ---- shared memory carve-up ----
     double* part = reinterpret_cast<double*>(smem_raw);                        // [SG*K][NT]
-    uint2* evl = reinterpret_cast<uint2*>(part + SG * K * kNT);                // [cap]
+    uint2* evl = reinterpret_cast<uint2*>(part + a.part_doubles);              // [cap]
     double* tab_mag = reinterpret_cast<double*>(evl + a.cap);                  // [entries] if tab_smem
     uint32_t* tab_info = reinterpret_cast<uint32_t*>(tab_mag + (a.tab_smem ? a.t.total_entries : 0));
     int* colstart = reinterpret_cast<int*>(tab_info + (a.tab_smem ? ((a.t.total_entries + 1) & ~1) : 0)); // [rw_max + 2]
@@ -166,6 +168,128 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
         if (n_events == 0) return;    // nobody moved within reach of this macro-tile
     } else {
         __syncthreads();
+    }
+
+    // ---- sparse tiles: event-centric scatter ------------------------------------------------
+    // With few movers in reach, walking events from every su wastes most lanes.  Instead the
+    // lanes enumerate (event, support offset, kind) triples — fully packed — and add each gated
+    // term to a per-address double in shared memory.  An address that receives ONE or TWO terms
+    // is order-independent: whichever StepCache slots they fall in, the reference's total is
+    // fl(t1 + t2) (IEEE addition is commutative, and 0.0 + t is exact), so a shared-memory atomic
+    // add reproduces it bit for bit.  Addresses with three or more terms (a few per cent of a
+    // sparse crowd) are recomputed by their owner thread through the exact K-slot walk.
+    if constexpr (ROWS == 2) {
+        if (single_pass && a.tab_smem && n_events <= a.ev_max) {
+            constexpr int CELLS = kTileW * MH;              // 256 su
+            double* acc = part;                             // [CELLS][24]   (part is 64 KB; this uses 48 KB)
+            uint32_t* cnt4 = reinterpret_cast<uint32_t*>(acc + CELLS * 24); // [CELLS*24/4] 8-bit term counts
+            uint32_t* touched = cnt4 + CELLS * 24 / 4;      // [CELLS] 24-bit address masks
+            {
+                float4* z = reinterpret_cast<float4*>(part);
+                constexpr int N16 = (CELLS * 24 * 8 + CELLS * 24 + CELLS * 4) / 16;
+                for (int i = tid; i < N16; i += kNT) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            __syncthreads();
+            const int IT = a.t.total_entries;
+            for (int r = lane; r < IT; r += 32) {
+                int kind = 0, rb = r;
+                while (kind < kKinds - 1 && rb >= a.t.k[kind].fw * a.t.k[kind].fh) {
+                    rb -= a.t.k[kind].fw * a.t.k[kind].fh;
+                    ++kind;
+                }
+                const uint32_t info = tab_info[r];
+                const uint32_t mask = (info >> 3) & 0xFFu;
+                if (mask == 0) continue; // offset outside the support (incl. the centre)
+                const KindTableDev& kt = a.t.k[kind];
+                const int dy = rb / kt.fw - kt.hh, dx = rb - (dy + kt.hh) * kt.fw - kt.hw;
+                const double mag = tab_mag[r];
+                const int sect = info & 7;
+                const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
+                for (int e = warp; e < n_events; e += kNW) {
+                    const uint2 evt = evl[e];
+                    const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su = mover - centre offset
+                    const int cy = (int)(evt.x >> 16) - dy - HH;
+                    if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
+                    const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
+                    const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                    const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
+                    if (!from && !to) continue;
+                    const int cell = cy * kTileW + cx;
+                    const int addr = cell * 24 + kind * kSects + sect;
+                    if (from) atomicAdd(&acc[addr], -mag);
+                    if (to) atomicAdd(&acc[addr], mag);
+                    atomicAdd(&cnt4[addr >> 2], ((from ? 1u : 0u) + (to ? 1u : 0u)) << (8 * (addr & 3)));
+                    atomicOr(&touched[cell], 1u << (kind * kSects + sect));
+                }
+            }
+            __syncthreads();
+            for (int cell = tid; cell < CELLS; cell += kNT) {
+                const uint32_t tmask = touched[cell];
+                if (tmask == 0) continue;
+                const int cx = cell % kTileW, cy = cell / kTileW;
+                const int tcx = cx + HW, tcy = cy + HH;
+                const long long gcell = cell_index(g, x0 + cx, y0 + cy);
+#pragma unroll 1
+                for (int kind = 0; kind < kKinds; ++kind) {
+                    const uint32_t km = (tmask >> (kind * kSects)) & 0xFFu;
+                    if (km == 0) continue;
+                    float4* rec = reinterpret_cast<float4*>(a.dyn + gcell * 24 + kind * kSects);
+                    const float4 v0 = rec[0], v1 = rec[1];
+                    float r[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                    const KindTableDev& kt = a.t.k[kind];
+                    int tbase = 0;
+                    for (int k = 0; k < kind; ++k) tbase += a.t.k[k].fw * a.t.k[k].fh;
+                    const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
+#pragma unroll
+                    for (int sect = 0; sect < kSects; ++sect) {
+                        if (!((km >> sect) & 1u)) continue;
+                        const int addr = cell * 24 + kind * kSects + sect;
+                        const uint32_t terms = (cnt4[addr >> 2] >> (8 * (addr & 3))) & 0xFFu;
+                        double total;
+                        if (terms <= 2u) {
+                            total = acc[addr];
+                        } else { // exact K-slot replay of this one address, events in list order
+                            double p[K];
+                            unsigned used = 0;
+                            for (int e = 0; e < n_events; ++e) {
+                                const uint2 evt = evl[e];
+                                const int dy = (int)(evt.x >> 16) - tcy, dx = (int)(evt.x & 0xFFFFu) - tcx;
+                                if (dy < -kt.hh || dy > kt.hh || dx < -kt.hw || dx > kt.hw || (dx | dy) == 0) continue;
+                                const int ti = tbase + (dy + kt.hh) * kt.fw + dx + kt.hw;
+                                const uint32_t info = tab_info[ti];
+                                const uint32_t mask = (info >> 3) & 0xFFu;
+                                if (mask == 0 || (int)(info & 7u) != sect) continue;
+                                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
+                                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
+                                const double mag = tab_mag[ti];
+                                const uint32_t j2 = (info >> 11) << 1;
+#pragma unroll
+                                for (int half = 0; half < 2; ++half) {
+                                    if (!(half == 0 ? from : to)) continue;
+                                    const int slot = (int)((j2 + half) & (K - 1));
+                                    const double term = half == 0 ? -mag : mag;
+#pragma unroll
+                                    for (int q = 0; q < K; ++q) {
+                                        if (q != slot) continue;
+                                        p[q] = ((used >> q) & 1u) ? __dadd_rn(p[q], term) : term;
+                                    }
+                                    used |= 1u << slot;
+                                }
+                            }
+                            total = 0.0;
+#pragma unroll
+                            for (int q = 0; q < K; ++q)
+                                if ((used >> q) & 1u) total = __dadd_rn(total, p[q]);
+                        }
+                        r[sect] = __fadd_rn(r[sect], __double2float_rn(total));
+                    }
+                    rec[0] = make_float4(r[0], r[1], r[2], r[3]);
+                    rec[1] = make_float4(r[4], r[5], r[6], r[7]);
+                }
+            }
+            return;
+        }
     }
 
     // Walks events [e0, e1) for the su (tcx, tcy) and one kind / sect group, adding each gated term
@@ -299,8 +423,11 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
 
 struct K5Shape {
     size_t smem;
-    int cap, rw_max, tab_smem;
+    int cap, rw_max, tab_smem, part_doubles;
 };
+
+// shared-memory bytes of the event-centric scatter: 256 su x 24 addresses x (double + count byte) + masks
+constexpr int kScatterBytes = 256 * 24 * 8 + 256 * 24 + 256 * 4;
 
 template <int K, int SG, int ROWS>
 K5Shape k5_shape(const TablesDev& t) {
@@ -314,7 +441,10 @@ K5Shape k5_shape(const TablesDev& t) {
     s.cap = (s.cap + 31) & ~31;
     s.tab_smem = t.total_entries <= kTabSmemMax;
     size_t b = 0;
-    b += sizeof(double) * SG * K * kNT;
+    size_t part_bytes = sizeof(double) * SG * K * kNT;
+    if (ROWS == 2 && s.tab_smem && part_bytes < (size_t)kScatterBytes) part_bytes = kScatterBytes;
+    s.part_doubles = (int)(part_bytes / sizeof(double));
+    b += part_bytes;
     b += sizeof(uint2) * (size_t)s.cap;
     if (s.tab_smem) b += sizeof(double) * t.total_entries + sizeof(uint32_t) * ((t.total_entries + 1) & ~1);
     b += sizeof(int) * (size_t)((s.rw_max + 2 + 1) & ~1);
@@ -338,6 +468,8 @@ cudaError_t launch_variant(cudaStream_t stream, const K5Launch& l) {
     a.cap = sh.cap;
     a.rw_max = sh.rw_max;
     a.tab_smem = sh.tab_smem;
+    a.part_doubles = sh.part_doubles;
+    a.ev_max = l.ev_max;
     const int tiles_y = (l.g.rows + MH - 1) / MH;
     const long long blocks = (long long)a.tiles_x * tiles_y;
     k5_writeback_kernel<K, SG, ROWS><<<(unsigned)blocks, kNT, sh.smem, stream>>>(a);

@@ -126,3 +126,19 @@ def test_against_compiled_reference(product_lib, ref_lib):
             np.testing.assert_array_equal(gpu.centers(), ref.centers())
             for k in range(3):
                 np.testing.assert_array_equal(bits(gpu.image(k)), bits(ref.image(k)))
+
+
+@pytest.mark.parametrize("knob", ["0", "100000"])
+@pytest.mark.parametrize("name", ["desk64", "k2", "k4", "k16", "field-5x9", "field-bigger-than-grid", "closed-four",
+                                  "wide-ragged", "d0.1-eight-ped1", "d0.9-four-ped3"])
+def test_both_k5_formulations(product_lib, monkeypatch, name, knob):
+    """k-5 has two formulations chosen per tile by the number of movers in reach: an event-centric
+    scatter (sparse tiles) and a su-centric gather (dense tiles).  SFC_K5_EVENT_MAX forces every
+    tile through one or the other; both must be bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_EVENT_MAX", knob)
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(4):
+        np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} knob {knob} tick {8 * (step + 1)}")
