@@ -43,6 +43,9 @@ struct sfc_engine {
     cudaGraphExec_t graph = nullptr;
     bool graph_valid = false;
 
+    int* dense_list = nullptr; // k-5 tile ids handed from the scatter to the gather kernel
+    int persistent_ctas = 148 * 3;
+    int k5_launches = 1;       // kernels per k-5 phase
     int k5_event_max = 64; // tuning knob, overridable with SFC_K5_EVENT_MAX (tests force either k-5 path)
     bool uploaded = false;
     long long tick = 0;
@@ -206,6 +209,8 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.chunk_k = e->cfg.chunk_k;
     l.advance_tick = advance;
     l.ev_max = e->k5_event_max;
+    l.dense_list = e->dense_list;
+    l.persistent_ctas = e->persistent_ctas;
     return l;
 }
 
@@ -329,6 +334,12 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(dev_alloc(&e->dyn, e->cells * kKinds * kSects), "cudaMalloc(dynamic images)");
     cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
     cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
+    cu(dev_alloc(&e->dense_list, k5_tile_count(e->g)), "cudaMalloc(dense tile list)");
+    {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->persistent_ctas = prop.multiProcessorCount * 3;
+        e->k5_launches = k5_kernels_per_launch(e->tabs, e->k5_event_max);
+    }
     if (rc != SFC_OK) return bail(rc);
     cu(cudaMemset(e->ctl, 0, sizeof(Ctl)), "cudaMemset");
     cu(cudaMemset(e->occ, 0xFF, sizeof(int) * (size_t)e->cells), "cudaMemset");
@@ -356,6 +367,7 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->dyn);
     cudaFree(e->ev);
     cudaFree(e->ctl);
+    cudaFree(e->dense_list);
     cudaFree(e->moved_counts);
     cudaFree(e->stage);
     cudaFree(e->dbg.enroll_ids);
@@ -509,7 +521,7 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
             SFC_CUDA(cudaGraphLaunch(e->graph, e->stream));
             e->counters.graph_launches += 1;
         }
-        e->counters.kernel_launches += 4;
+        e->counters.kernel_launches += 3 + e->k5_launches;
         if (interval > 0 && (base + t + 1) % interval == 0) {
             rc = enqueue_rebuild(e);
             if (rc != SFC_OK) return rc;
@@ -579,7 +591,7 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
             break;
         case 5:
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 0)));
-            e->counters.kernel_launches += 1;
+            e->counters.kernel_launches += e->k5_launches;
             break;
         case 6: {
             SFC_CUDA(launch_tick_advance(e->stream, e->ctl));

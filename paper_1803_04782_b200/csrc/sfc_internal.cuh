@@ -114,7 +114,7 @@ struct Ctl {
     int error_x, error_y;
     double error_value;
     unsigned int drift_bits[kKinds]; // max |old - fresh| per kind as float bits (rebuild)
-    int pad;
+    int dense_count;         // k-5: tiles the scatter kernel handed to the gather kernel this tick
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -161,6 +161,8 @@ struct K5Launch {
     int chunk_k;
     int advance_tick; // fold "tick += 1" into the kernel (fast path)
     int ev_max;       // k-5: event-count threshold between the scatter and the gather formulation
+    int* dense_list;  // k-5: tile ids for the gather kernel (k5_tile_count entries), or nullptr
+    int persistent_ctas; // k-5: grid of the persistent gather kernel
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp);
@@ -169,7 +171,8 @@ cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p,
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
                            unsigned long long* moved_counts, const DebugArrays& dbg);
 cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& a);
-size_t k5_smem_bytes(int chunk_k, const TablesDev& t);
+int k5_kernels_per_launch(const TablesDev& t, int ev_max);
+long long k5_tile_count(const GridDev& g);
 
 // rebuild / rasterize_dynamic.  mode 0: write fresh images to `out` (record layout), no compare;
 // mode 1: compare with dyn and record the per-kind drift maxima in ctl; mode 2: overwrite dyn

@@ -7,31 +7,40 @@
 // doubles through a K-slot StepCache (term idx -> slot idx mod K, accumulator.hpp:36-46), fold
 // the K slots in slot order, cast to float, add to the image.  6F mask probes per su.
 //
-// B200 formulation (bit-identical results):
-//   * One CTA (4 warps) owns a macro-tile of 32 x (4*ROWS) su.  It stages the macro-tile +
-//     field-halo region of the 2-byte event map in shared memory ONCE (coalesced row reads) and
-//     compacts the (few) movement events into a list ordered by (x, then y) with warp ballots —
-//     no atomics.  That order equals the reference's contributor-list order for every target in
-//     the tile, because the lists are sorted lexicographically by centre offset
-//     (fields.hpp:55-57): walking the list front to back feeds every StepCache slot its terms in
-//     the reference's order.  Zero terms are never materialised (adding +-0.0 to a partial cannot
-//     change it), so the work is proportional to the number of movers, not to the field area.
-//   * A warp owns one row of 32 su at a time, one su per lane, and walks the event list with a
-//     warp-uniform trip count (events are filtered by row distance, which is the same for all
-//     lanes); only the per-lane "is this offset in the support, which sect, which slot" part
-//     diverges.  The K x 8 double partials of the kind being processed live in shared memory laid
-//     out [slot][thread] (bank = lane: conflict-free for any per-lane slot) and are created
-//     lazily under a 64-bit dirty mask, so untouched addresses cost nothing and the fold visits
-//     only dirty slots (ascending bit order = slot order).
-//   * Only su that received a term touch HBM: one 32-byte sector per (su, kind), read with the
-//     walk still in flight and written back after the fold.  Nothing is read or written for su
-//     out of every mover's reach, so sparse crowds move far fewer than the dense 192 B/su.
+// B200 formulation (bit-identical results).  A CTA owns a tile of 32 x 8 su.  It stages the tile +
+// field-halo region of the 2-byte event map in shared memory once (coalesced row reads) and
+// compacts the (few) movement events into a list ordered by (x, then y) with warp ballots — no
+// atomics.  That order equals the reference's contributor-list order for every target in the
+// tile, because the lists are sorted lexicographically by centre offset (fields.hpp:55-57).
+// Zero terms are never materialised (adding +-0.0 to a partial cannot change it), so the work
+// is proportional to the number of movers, not to the field area.  Two formulations follow,
+// chosen per tile by the number of events in reach:
+//
+//   SCATTER (sparse tiles, 256 threads): lanes enumerate (event, support offset, kind) triples —
+//     fully packed — and add each gated term to a per-address double in shared memory.  An
+//     address that receives ONE or TWO terms is order-independent: whichever StepCache slots
+//     they fall in, the reference's total is fl(t1 + t2) (IEEE addition is commutative and
+//     0.0 + t is exact), so a shared-memory atomic add reproduces it bit for bit.  Addresses with
+//     three or more terms (a few per cent of a sparse crowd) go on a work list and are replayed
+//     through the exact K-slot order, one address per thread.  Tiles with too many events are
+//     appended to a device-side list for the second kernel.
+//
+//   GATHER (dense tiles, 128 threads, persistent over that list): a warp owns a block of 8 x 4 su,
+//     one su per lane, and walks the events in reach with a warp-uniform trip count; only the
+//     per-lane "is this offset in the support, which sect, which slot" part diverges.  The K x 8
+//     double partials of the kind being processed live in shared memory laid out [slot][thread]
+//     (bank = lane: conflict-free for any per-lane slot) and are created lazily under a 64-bit
+//     dirty mask; the fold visits only dirty slots (ascending bit order = slot order).
+//
+// In both, only su that received a term touch HBM: one 32-byte sector per (su, kind).  Nothing is
+// read or written for su out of every mover's reach, so sparse crowds move far fewer than the
+// dense 192 B/su.
 //
 // Fields larger than the grid wrap onto themselves (test_engine.cpp:329-340): the region is
 // scanned in unwrapped coordinates, so one physical su can appear several times, once per
 // periodic image — exactly the reference's while-loop wraps (engine.cpp:450-454).
-// Regions too large for shared memory (very large fields) are processed in column chunks
-// (ROWS = 1 only): the list is sorted, so chunks arrive in order.
+// Regions too large for shared memory (very large fields) use 32 x 4 tiles, gather only, with the
+// region staged in column chunks: the list is sorted, so chunks arrive in order.
 
 #include "sfc_internal.cuh"
 
@@ -40,11 +49,15 @@ namespace sfc {
 namespace {
 
 constexpr int kTileW = 32;
-constexpr int kNT = 128;              // threads per CTA
-constexpr int kNW = kNT / 32;         // warps
-constexpr int kBlockW = 8, kBlockH = 4; // su block owned by one warp at a time (one su per lane)
-constexpr int kChunkCells = 2048;     // region cells staged per pass (codes 4 KB + list 16 KB)
-constexpr int kTabSmemMax = 768;      // table entries (all kinds) kept in shared memory
+constexpr int kBlockW = 8, kBlockH = 4; // su block owned by one warp at a time in the gather (one su per lane)
+constexpr int kChunkCells = 2048;       // region cells staged per pass (codes 4 KB + list 16 KB)
+constexpr int kTabSmemMax = 768;        // table entries (all kinds) kept in shared memory
+constexpr int kReplayCap = 1020;        // scatter: work-list capacity for addresses with >= 3 terms
+constexpr int kScatterCells = 256;      // scatter tile = 32 x 8 su
+// shared-memory bytes of the scatter: su x 24 addresses x (double + count byte) + masks + work list
+constexpr int kScatterBytes = kScatterCells * 24 * 8 + kScatterCells * 24 + kScatterCells * 4 + (kReplayCap + 4) * 4;
+
+enum { kModeAll = 0, kModeScatter = 1, kModeDense = 2 };
 
 struct K5Args {
     GridDev g;
@@ -52,57 +65,62 @@ struct K5Args {
     float* dyn;
     const uint8_t* ev;
     Ctl* ctl;
+    int* dense_list;
     int tiles_x;
     int advance_tick;
-    int cap;       // cells staged per pass = event-list capacity
-    int rw_max;    // region columns for a full tile
-    int tab_smem;  // contributor tables fit in shared memory
+    int cap;          // cells staged per pass = event-list capacity
+    int rw_max;       // region columns for a full tile
+    int tab_smem;     // contributor tables fit in shared memory
     int part_doubles; // size of the partial-sum / scatter region, in doubles
-    int ev_max;    // tiles with at most this many events in reach take the event-centric path
+    int ev_max;       // scatter handles tiles with at most this many events in reach
 };
 
-// K: StepCache width.  SG: sects accumulated per walk (SG * K <= 64: the dirty set is one 64-bit
-// word).  ROWS: tile rows each warp processes in turn (macro-tile height = 4 * ROWS).
-template <int K, int SG, int ROWS>
-__global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
+struct Smem {
+    double* part;
+    uint2* evl;
+    double* tab_mag;
+    uint32_t* tab_info;
+    int* colstart;
+    uint16_t* codes;
+};
+
+__device__ __forceinline__ Smem carve(unsigned char* raw, const K5Args& a) {
+    Smem s;
+    s.part = reinterpret_cast<double*>(raw);
+    s.evl = reinterpret_cast<uint2*>(s.part + a.part_doubles);
+    s.tab_mag = reinterpret_cast<double*>(s.evl + a.cap);
+    s.tab_info = reinterpret_cast<uint32_t*>(s.tab_mag + (a.tab_smem ? a.t.total_entries : 0));
+    s.colstart = reinterpret_cast<int*>(s.tab_info + (a.tab_smem ? ((a.t.total_entries + 1) & ~1) : 0));
+    s.codes = reinterpret_cast<uint16_t*>(s.colstart + ((a.rw_max + 2 + 1) & ~1));
+    return s;
+}
+
+// K: StepCache width.  SG: sects accumulated per gather walk (SG * K <= 64: the dirty set is one
+// 64-bit word).  ROWS: block rows per tile (tile height = 4 * ROWS).  NT: threads.
+template <int K, int SG, int ROWS, int NT, int MODE>
+__device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
+    constexpr int NW = NT / 32;
     constexpr int NG = kSects / SG;
-    constexpr int MH = kNW * ROWS;
+    constexpr int MH = kBlockH * ROWS;
     static_assert(SG * K <= 64, "dirty mask is one 64-bit word");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
 
     const GridDev g = a.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
-    if (a.ctl->error_code != 0) return;
+    double* const part = sm.part;
+    uint2* const evl = sm.evl;
+    int* const colstart = sm.colstart;
+    uint16_t* const codes = sm.codes;
+    const double* const tab_mag = sm.tab_mag;
+    const uint32_t* const tab_info = sm.tab_info;
 
-    // ---- shared memory carve-up ----
-    double* part = reinterpret_cast<double*>(smem_raw);                        // [SG*K][NT]
-    uint2* evl = reinterpret_cast<uint2*>(part + a.part_doubles);              // [cap]
-    double* tab_mag = reinterpret_cast<double*>(evl + a.cap);                  // [entries] if tab_smem
-    uint32_t* tab_info = reinterpret_cast<uint32_t*>(tab_mag + (a.tab_smem ? a.t.total_entries : 0));
-    int* colstart = reinterpret_cast<int*>(tab_info + (a.tab_smem ? ((a.t.total_entries + 1) & ~1) : 0)); // [rw_max + 2]
-    uint16_t* codes = reinterpret_cast<uint16_t*>(colstart + ((a.rw_max + 2 + 1) & ~1)); // [cap] column-major
-
-    const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
+    const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
     const int x0 = tile_x * kTileW;
-    const int y0 = g.row0 + tile_y * MH; // global row of the macro-tile's first row
+    const int y0 = g.row0 + tile_y * MH; // global row of the tile's first row
     const int nx = min(kTileW, g.W - x0);
     const int ny = min(MH, g.row0 + g.rows - y0);
     const int HW = a.t.max_hw, HH = a.t.max_hh;
     const int RW = nx + 2 * HW, RH = ny + 2 * HH;
     const int xs = x0 - HW, ys = y0 - HH;
-
-    if (a.tab_smem) {
-        int base = 0;
-        for (int k = 0; k < kKinds; ++k) {
-            const int n = a.t.k[k].fw * a.t.k[k].fh;
-            for (int i = tid; i < n; i += kNT) {
-                tab_mag[base + i] = a.t.k[k].mag[i];
-                tab_info[base + i] = a.t.k[k].info[i];
-            }
-            base += n;
-        }
-    }
 
     const uint16_t* ev16 = reinterpret_cast<const uint16_t*>(a.ev);
     const int cols_per_pass = max(1, a.cap / RH);
@@ -113,15 +131,27 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
     // Returns the event count (uniform across the CTA).
     auto build_list = [&](int c0, int c1) -> int {
         const int ncols = c1 - c0;
-        for (int ry = warp; ry < RH; ry += kNW) {
-            const int gy = ys + ry;
+        const bool narrow = RW <= g.W; // one conditional add wraps x (wider regions take the general path)
+        for (int ry = warp; ry < RH; ry += NW) {
+            const long long row = cell_index(g, 0, ys + ry); // uniform per warp; -1: row does not exist
             for (int rc = lane; rc < ncols; rc += 32) {
-                const long long idx = cell_index(g, xs + c0 + rc, gy);
-                codes[rc * RH + ry] = idx >= 0 ? ev16[idx] : (uint16_t)0;
+                int x = xs + c0 + rc;
+                long long idx = -1;
+                if (narrow) {
+                    if (g.closed) {
+                        if (row >= 0 && x >= 0 && x < g.W) idx = row + x;
+                    } else if (row >= 0) {
+                        x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
+                        idx = row + x;
+                    }
+                } else {
+                    idx = cell_index(g, x, ys + ry);
+                }
+                codes[rc * RH + ry] = idx >= 0 ? __ldg(ev16 + idx) : (uint16_t)0;
             }
         }
         __syncthreads();
-        for (int rc = warp; rc < ncols; rc += kNW) { // per-column counts
+        for (int rc = warp; rc < ncols; rc += NW) { // per-column counts
             int cnt = 0;
             for (int r0 = 0; r0 < RH; r0 += 32) {
                 const int ry = r0 + lane;
@@ -146,7 +176,7 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
             }
         }
         __syncthreads();
-        for (int rc = warp; rc < ncols; rc += kNW) {
+        for (int rc = warp; rc < ncols; rc += NW) {
             int pos = colstart[rc];
             if (colstart[rc + 1] == pos) continue;
             for (int r0 = 0; r0 < RH; r0 += 32) {
@@ -164,260 +194,317 @@ __global__ void __launch_bounds__(kNT) k5_writeback_kernel(K5Args a) {
 
     int n_events = 0;
     if (single_pass) {
-        n_events = build_list(0, RW); // also orders the table copy above before its first use
-        if (n_events == 0) return;    // nobody moved within reach of this macro-tile
-    } else {
-        __syncthreads();
+        n_events = build_list(0, RW);
+        if (n_events == 0) return; // nobody moved within reach of this tile
     }
 
-    // ---- sparse tiles: event-centric scatter ------------------------------------------------
-    // With few movers in reach, walking events from every su wastes most lanes.  Instead the
-    // lanes enumerate (event, support offset, kind) triples — fully packed — and add each gated
-    // term to a per-address double in shared memory.  An address that receives ONE or TWO terms
-    // is order-independent: whichever StepCache slots they fall in, the reference's total is
-    // fl(t1 + t2) (IEEE addition is commutative, and 0.0 + t is exact), so a shared-memory atomic
-    // add reproduces it bit for bit.  Addresses with three or more terms (a few per cent of a
-    // sparse crowd) are recomputed by their owner thread through the exact K-slot walk.
-    if constexpr (ROWS == 2) {
-        if (single_pass && a.tab_smem && n_events <= a.ev_max) {
-            constexpr int CELLS = kTileW * MH;              // 256 su
-            double* acc = part;                             // [CELLS][24]   (part is 64 KB; this uses 48 KB)
-            uint32_t* cnt4 = reinterpret_cast<uint32_t*>(acc + CELLS * 24); // [CELLS*24/4] 8-bit term counts
-            uint32_t* touched = cnt4 + CELLS * 24 / 4;      // [CELLS] 24-bit address masks
-            {
-                float4* z = reinterpret_cast<float4*>(part);
-                constexpr int N16 = (CELLS * 24 * 8 + CELLS * 24 + CELLS * 4) / 16;
-                for (int i = tid; i < N16; i += kNT) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            __syncthreads();
-            const int IT = a.t.total_entries;
-            for (int r = lane; r < IT; r += 32) {
-                int kind = 0, rb = r;
-                while (kind < kKinds - 1 && rb >= a.t.k[kind].fw * a.t.k[kind].fh) {
-                    rb -= a.t.k[kind].fw * a.t.k[kind].fh;
-                    ++kind;
-                }
-                const uint32_t info = tab_info[r];
-                const uint32_t mask = (info >> 3) & 0xFFu;
-                if (mask == 0) continue; // offset outside the support (incl. the centre)
-                const KindTableDev& kt = a.t.k[kind];
-                const int dy = rb / kt.fw - kt.hh, dx = rb - (dy + kt.hh) * kt.fw - kt.hw;
-                const double mag = tab_mag[r];
-                const int sect = info & 7;
-                const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
-                for (int e = warp; e < n_events; e += kNW) {
-                    const uint2 evt = evl[e];
-                    const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su = mover - centre offset
-                    const int cy = (int)(evt.x >> 16) - dy - HH;
-                    if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
-                    const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
-                    const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-                    const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
-                    if (!from && !to) continue;
-                    const int cell = cy * kTileW + cx;
-                    const int addr = cell * 24 + kind * kSects + sect;
-                    if (from) atomicAdd(&acc[addr], -mag);
-                    if (to) atomicAdd(&acc[addr], mag);
-                    atomicAdd(&cnt4[addr >> 2], ((from ? 1u : 0u) + (to ? 1u : 0u)) << (8 * (addr & 3)));
-                    atomicOr(&touched[cell], 1u << (kind * kSects + sect));
-                }
-            }
-            __syncthreads();
-            for (int cell = tid; cell < CELLS; cell += kNT) {
-                const uint32_t tmask = touched[cell];
-                if (tmask == 0) continue;
-                const int cx = cell % kTileW, cy = cell / kTileW;
-                const int tcx = cx + HW, tcy = cy + HH;
-                const long long gcell = cell_index(g, x0 + cx, y0 + cy);
-#pragma unroll 1
-                for (int kind = 0; kind < kKinds; ++kind) {
-                    const uint32_t km = (tmask >> (kind * kSects)) & 0xFFu;
-                    if (km == 0) continue;
-                    float4* rec = reinterpret_cast<float4*>(a.dyn + gcell * 24 + kind * kSects);
-                    const float4 v0 = rec[0], v1 = rec[1];
-                    float r[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                    const KindTableDev& kt = a.t.k[kind];
-                    int tbase = 0;
-                    for (int k = 0; k < kind; ++k) tbase += a.t.k[k].fw * a.t.k[k].fh;
-                    const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
-#pragma unroll
-                    for (int sect = 0; sect < kSects; ++sect) {
-                        if (!((km >> sect) & 1u)) continue;
-                        const int addr = cell * 24 + kind * kSects + sect;
-                        const uint32_t terms = (cnt4[addr >> 2] >> (8 * (addr & 3))) & 0xFFu;
-                        double total;
-                        if (terms <= 2u) {
-                            total = acc[addr];
-                        } else { // exact K-slot replay of this one address, events in list order
-                            double p[K];
-                            unsigned used = 0;
-                            for (int e = 0; e < n_events; ++e) {
-                                const uint2 evt = evl[e];
-                                const int dy = (int)(evt.x >> 16) - tcy, dx = (int)(evt.x & 0xFFFFu) - tcx;
-                                if (dy < -kt.hh || dy > kt.hh || dx < -kt.hw || dx > kt.hw || (dx | dy) == 0) continue;
-                                const int ti = tbase + (dy + kt.hh) * kt.fw + dx + kt.hw;
-                                const uint32_t info = tab_info[ti];
-                                const uint32_t mask = (info >> 3) & 0xFFu;
-                                if (mask == 0 || (int)(info & 7u) != sect) continue;
-                                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
-                                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-                                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
-                                const double mag = tab_mag[ti];
-                                const uint32_t j2 = (info >> 11) << 1;
-#pragma unroll
-                                for (int half = 0; half < 2; ++half) {
-                                    if (!(half == 0 ? from : to)) continue;
-                                    const int slot = (int)((j2 + half) & (K - 1));
-                                    const double term = half == 0 ? -mag : mag;
-#pragma unroll
-                                    for (int q = 0; q < K; ++q) {
-                                        if (q != slot) continue;
-                                        p[q] = ((used >> q) & 1u) ? __dadd_rn(p[q], term) : term;
-                                    }
-                                    used |= 1u << slot;
-                                }
-                            }
-                            total = 0.0;
-#pragma unroll
-                            for (int q = 0; q < K; ++q)
-                                if ((used >> q) & 1u) total = __dadd_rn(total, p[q]);
-                        }
-                        r[sect] = __fadd_rn(r[sect], __double2float_rn(total));
-                    }
-                    rec[0] = make_float4(r[0], r[1], r[2], r[3]);
-                    rec[1] = make_float4(r[4], r[5], r[6], r[7]);
-                }
-            }
+    // =========================================================================================
+    // SCATTER
+    // =========================================================================================
+    if constexpr (MODE == kModeScatter) {
+        if (n_events > a.ev_max) { // dense tile: hand it to the gather kernel
+            if (tid == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
             return;
         }
-    }
-
-    // Walks events [e0, e1) for the su (tcx, tcy) and one kind / sect group, adding each gated term
-    // to its StepCache slot.  The loop trip count and the row filter are warp-uniform.
-    auto walk = [&](int e0, int e1, int kind, int sg, const KindTableDev& kt, const double* kmag,
-                    const uint32_t* kinfo, int tcx, int tcy, int by0r, unsigned long long& dirty) {
-        const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
-        for (int e = e0; e < e1; ++e) {
-            const uint2 evt = evl[e];                 // broadcast read
-            const int ery = (int)(evt.x >> 16);
-            if (ery < by0r - kt.hh || ery > by0r + kBlockH - 1 + kt.hh) continue; // uniform: out of the block's reach
-            const int dy = ery - tcy;
-            const int dx = (int)(evt.x & 0xFFFFu) - tcx;
-            if (dy < -kt.hh || dy > kt.hh || dx < -kt.hw || dx > kt.hw || (dx | dy) == 0) continue;
-            const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
-            const uint32_t info = kinfo[ti];
+        constexpr int CELLS = kScatterCells;
+        double* acc = part;                                                  // [CELLS][24]
+        uint32_t* cnt4 = reinterpret_cast<uint32_t*>(acc + CELLS * 24);      // [CELLS*24/4] 8-bit term counts
+        uint32_t* touched = cnt4 + CELLS * 24 / 4;                           // [CELLS] 24-bit address masks
+        int* replay = reinterpret_cast<int*>(touched + CELLS);               // [kReplayCap]
+        int* n_replay = replay + kReplayCap;
+        {
+            float4* z = reinterpret_cast<float4*>(part);
+            constexpr int N16 = (CELLS * 24 * 8 + CELLS * 24 + CELLS * 4) / 16;
+            for (int i = tid; i < N16; i += NT) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (tid == 0) *n_replay = 0;
+        }
+        __syncthreads();
+        const int IT = a.t.total_entries;
+        for (int r = lane; r < IT; r += 32) {
+            int kind = 0, rb = r;
+            while (kind < kKinds - 1 && rb >= a.t.k[kind].fw * a.t.k[kind].fh) {
+                rb -= a.t.k[kind].fw * a.t.k[kind].fh;
+                ++kind;
+            }
+            const uint32_t info = tab_info[r];
             const uint32_t mask = (info >> 3) & 0xFFu;
-            if (mask == 0) continue;
+            if (mask == 0) continue; // offset outside the support (incl. the centre)
+            const KindTableDev& kt = a.t.k[kind];
+            const int dy = rb / kt.fw - kt.hh, dx = rb - (dy + kt.hh) * kt.fw - kt.hw;
+            const double mag = tab_mag[r];
             const int sect = info & 7;
-            if (SG < kSects && sect / SG != sg) continue;
-            const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
-            const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-            const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
-            if (!from && !to) continue;
-            const double mag = kmag[ti];
-            const uint32_t j2 = (info >> 11) << 1;
-            const int ls = sect % SG;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) { // from-term (idx 2j) then to-term (idx 2j+1)
-                if (!(half == 0 ? from : to)) continue;
-                const int addr = ls * K + (int)((j2 + half) & (K - 1));
-                const unsigned long long bit = 1ull << addr;
-                double* cellp = part + addr * kNT + tid;
-                const double term = half == 0 ? -mag : mag;
-                if (dirty & bit) {
-                    *cellp = __dadd_rn(*cellp, term);
-                } else {
-                    *cellp = term; // 0.0 + term
-                    dirty |= bit;
-                }
+            const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
+            for (int e = warp; e < n_events; e += NW) {
+                const uint2 evt = evl[e];
+                const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su = mover - centre offset
+                const int cy = (int)(evt.x >> 16) - dy - HH;
+                if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
+                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
+                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
+                if (!from && !to) continue;
+                const int cell = cy * kTileW + cx;
+                const int addr = cell * 24 + kind * kSects + sect;
+                if (from) atomicAdd(&acc[addr], -mag);
+                if (to) atomicAdd(&acc[addr], mag);
+                atomicAdd(&cnt4[addr >> 2], ((from ? 1u : 0u) + (to ? 1u : 0u)) << (8 * (addr & 3)));
+                atomicOr(&touched[cell], 1u << (kind * kSects + sect));
             }
         }
-    };
-
-    // Folds the dirty slots of one (kind, sect group) into the su's image sector:
-    // StepCache::total in slot order (accumulator.hpp:41-46), then image += (float)total.
-    auto fold = [&](unsigned long long dirty, float* r) {
-        while (dirty != 0ull) {
-            const int first = __ffsll((long long)dirty) - 1;
-            const int ls = first / K;
-            const unsigned long long group = dirty & (((1ull << K) - 1ull) << (ls * K));
-            dirty &= ~group;
-            unsigned long long rest = group;
-            double total = 0.0;
-            while (rest != 0ull) {
-                const int addr = __ffsll((long long)rest) - 1;
-                rest &= rest - 1ull;
-                total = __dadd_rn(total, part[addr * kNT + tid]);
-            }
-            const float add = __double2float_rn(total);
+        __syncthreads();
+        // addresses with three or more terms: exact K-slot replay, one address per thread
+        for (int w = tid; w < CELLS * 24 / 4; w += NT) {
+            const uint32_t v = cnt4[w];
+            if ((v + 0x7D7D7D7Du) & 0x80808080u) { // some byte > 2 (counts stay below 0x80)
 #pragma unroll
-            for (int q = 0; q < SG; ++q)
-                if (q == ls) r[q] = __fadd_rn(r[q], add);
+                for (int b = 0; b < 4; ++b)
+                    if (((v >> (8 * b)) & 0xFFu) > 2u) {
+                        const int slot = atomicAdd(n_replay, 1);
+                        if (slot < kReplayCap) replay[slot] = w * 4 + b;
+                    }
+            }
         }
-    };
-
-#pragma unroll 1
-    for (int rr = 0; rr < ROWS; ++rr) {
-        // this warp's block of 8 x 4 su: four blocks side by side, ROWS block rows per macro-tile
-        const int bx = warp * kBlockW, by = rr * kBlockH;
-        const bool blk_ok = by < ny && bx < nx; // uniform per warp
-        if (single_pass && !blk_ok) continue;   // (chunked mode keeps every warp in the CTA-wide list builds)
-        const int cx = bx + (lane % kBlockW), cy = by + (lane / kBlockW); // my su in the macro-tile
-        const int tcx = cx + HW, tcy = cy + HH;                             // ... in region coordinates
-        const bool in_grid = blk_ok && cx < nx && cy < ny;
-        const long long cell = in_grid ? cell_index(g, x0 + cx, y0 + cy) : -1;
-        float4* rec = reinterpret_cast<float4*>(a.dyn + (cell < 0 ? 0 : cell) * 24);
-        // events that can reach the block lie in a contiguous range of the x-sorted list
-        int e_lo = 0, e_hi = n_events;
-        if (single_pass) {
-            e_lo = colstart[max(bx, 0)];
-            e_hi = colstart[min(bx + kBlockW + 2 * HW, RW)];
-            if (e_lo == e_hi) continue; // uniform
-        }
-
-#pragma unroll 1
-        for (int kind = 0; kind < kKinds; ++kind) {
-            const KindTableDev kt = a.t.k[kind];
+        __syncthreads();
+        const int n_rep = *n_replay;
+        const bool overflow = n_rep > kReplayCap; // then every thread scans the addresses for its share
+        const int rep_items = overflow ? CELLS * 24 : n_rep;
+        for (int i = tid; i < rep_items; i += NT) {
+            const int addr = overflow ? i : replay[i];
+            if (overflow && ((cnt4[addr >> 2] >> (8 * (addr & 3))) & 0xFFu) <= 2u) continue;
+            const int cell = addr / 24, kind = (addr % 24) / kSects, sect = addr % kSects;
+            const int tcx = cell % kTileW + HW, tcy = cell / kTileW + HH;
+            const KindTableDev& kt = a.t.k[kind];
             int tbase = 0;
             for (int k = 0; k < kind; ++k) tbase += a.t.k[k].fw * a.t.k[k].fh;
-            const double* kmag = a.tab_smem ? tab_mag + tbase : kt.mag;
-            const uint32_t* kinfo = a.tab_smem ? tab_info + tbase : kt.info;
+            const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
+            double p[K];
+            unsigned used = 0;
+            for (int e = 0; e < n_events; ++e) { // events in list order = contributor order
+                const uint2 evt = evl[e];
+                const int dy = (int)(evt.x >> 16) - tcy, dx = (int)(evt.x & 0xFFFFu) - tcx;
+                if (dy < -kt.hh || dy > kt.hh || dx < -kt.hw || dx > kt.hw || (dx | dy) == 0) continue;
+                const int ti = tbase + (dy + kt.hh) * kt.fw + dx + kt.hw;
+                const uint32_t info = tab_info[ti];
+                const uint32_t mask = (info >> 3) & 0xFFu;
+                if (mask == 0 || (int)(info & 7u) != sect) continue;
+                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
+                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
+                const double mag = tab_mag[ti];
+                const uint32_t j2 = (info >> 11) << 1;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) { // from-term (idx 2j) then to-term (idx 2j+1)
+                    if (!(half == 0 ? from : to)) continue;
+                    const int slot = (int)((j2 + half) & (K - 1));
+                    const double term = half == 0 ? -mag : mag;
+#pragma unroll
+                    for (int q = 0; q < K; ++q) {
+                        if (q != slot) continue;
+                        p[q] = ((used >> q) & 1u) ? __dadd_rn(p[q], term) : term;
+                    }
+                    used |= 1u << slot;
+                }
+            }
+            double total = 0.0; // StepCache::total, slot order
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                if ((used >> q) & 1u) total = __dadd_rn(total, p[q]);
+            acc[addr] = total;
+        }
+        __syncthreads();
+        // apply: one 32-byte sector per touched (su, kind); every load of a thread is issued before
+        // the first is consumed
+        constexpr int PAIRS = CELLS * kKinds / NT;
+        float4 v[PAIRS][2];
+        uint32_t km[PAIRS];
+        float4* rec[PAIRS];
+#pragma unroll
+        for (int q = 0; q < PAIRS; ++q) {
+            const int pr = q * NT + tid, kind = pr / CELLS, cell = pr % CELLS;
+            km[q] = (touched[cell] >> (kind * kSects)) & 0xFFu;
+            rec[q] = nullptr;
+            if (km[q] != 0) {
+                const long long gcell = cell_index(g, x0 + cell % kTileW, y0 + cell / kTileW);
+                rec[q] = reinterpret_cast<float4*>(a.dyn + gcell * 24 + kind * kSects);
+                v[q][0] = rec[q][0];
+                v[q][1] = rec[q][1];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < PAIRS; ++q) {
+            if (km[q] == 0) continue;
+            const int pr = q * NT + tid, kind = pr / CELLS, cell = pr % CELLS;
+            const double* ap = acc + cell * 24 + kind * kSects;
+            float r[8] = {v[q][0].x, v[q][0].y, v[q][0].z, v[q][0].w, v[q][1].x, v[q][1].y, v[q][1].z, v[q][1].w};
+#pragma unroll
+            for (int sect = 0; sect < kSects; ++sect)
+                if ((km[q] >> sect) & 1u) r[sect] = __fadd_rn(r[sect], __double2float_rn(ap[sect])); // image += (float)total
+            rec[q][0] = make_float4(r[0], r[1], r[2], r[3]);
+            rec[q][1] = make_float4(r[4], r[5], r[6], r[7]);
+        }
+        return;
+    } else {
+        // =====================================================================================
+        // GATHER
+        // =====================================================================================
+        // Walks events [e0, e1) for the su (tcx, tcy) and one kind / sect group, adding each gated
+        // term to its StepCache slot.  The loop trip count and the block filter are warp-uniform.
+        auto walk = [&](int e0, int e1, int kind, int sg, const KindTableDev& kt, const double* kmag,
+                        const uint32_t* kinfo, int tcx, int tcy, int by0r, unsigned long long& dirty) {
+            const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8);
+            for (int e = e0; e < e1; ++e) {
+                const uint2 evt = evl[e]; // broadcast read
+                const int ery = (int)(evt.x >> 16);
+                if (ery < by0r - kt.hh || ery > by0r + kBlockH - 1 + kt.hh) continue; // uniform: out of the block's reach
+                const int dy = ery - tcy;
+                const int dx = (int)(evt.x & 0xFFFFu) - tcx;
+                if (dy < -kt.hh || dy > kt.hh || dx < -kt.hw || dx > kt.hw || (dx | dy) == 0) continue;
+                const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
+                const uint32_t info = kinfo[ti];
+                const uint32_t mask = (info >> 3) & 0xFFu;
+                if (mask == 0) continue;
+                const int sect = info & 7;
+                if (SG < kSects && sect / SG != sg) continue;
+                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
+                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
+                if (!from && !to) continue;
+                const double mag = kmag[ti];
+                const uint32_t j2 = (info >> 11) << 1;
+                const int ls = sect % SG;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) { // from-term (idx 2j) then to-term (idx 2j+1)
+                    if (!(half == 0 ? from : to)) continue;
+                    const int addr = ls * K + (int)((j2 + half) & (K - 1));
+                    const unsigned long long bit = 1ull << addr;
+                    double* cellp = part + addr * NT + tid;
+                    const double term = half == 0 ? -mag : mag;
+                    if (dirty & bit) {
+                        *cellp = __dadd_rn(*cellp, term);
+                    } else {
+                        *cellp = term; // 0.0 + term
+                        dirty |= bit;
+                    }
+                }
+            }
+        };
+
+        // Folds the dirty slots of one (kind, sect group) into the su's image sector:
+        // StepCache::total in slot order (accumulator.hpp:41-46), then image += (float)total.
+        auto fold = [&](unsigned long long dirty, float* r) {
+            while (dirty != 0ull) {
+                const int first = __ffsll((long long)dirty) - 1;
+                const int ls = first / K;
+                const unsigned long long group = dirty & (((1ull << K) - 1ull) << (ls * K));
+                dirty &= ~group;
+                unsigned long long rest = group;
+                double total = 0.0;
+                while (rest != 0ull) {
+                    const int addr = __ffsll((long long)rest) - 1;
+                    rest &= rest - 1ull;
+                    total = __dadd_rn(total, part[addr * NT + tid]);
+                }
+                const float add = __double2float_rn(total);
+#pragma unroll
+                for (int q = 0; q < SG; ++q)
+                    if (q == ls) r[q] = __fadd_rn(r[q], add);
+            }
+        };
+
+        constexpr int NBLK = 4 * ROWS; // 8 x 4 blocks per tile: four side by side, ROWS deep
 #pragma unroll 1
-            for (int sg = 0; sg < NG; ++sg) {
-                unsigned long long dirty = 0ull;
-                if (single_pass) {
-                    if (in_grid) walk(e_lo, e_hi, kind, sg, kt, kmag, kinfo, tcx, tcy, by + HH, dirty);
-                } else { // ROWS == 1: chunked region, list rebuilt per (kind, group)
-                    for (int c0 = 0; c0 < RW; c0 += cols_per_pass) {
-                        const int n = build_list(c0, min(RW, c0 + cols_per_pass));
-                        if (n > 0 && in_grid) walk(0, n, kind, sg, kt, kmag, kinfo, tcx, tcy, by + HH, dirty);
-                        __syncthreads();
+        for (int b0 = 0; b0 < NBLK; b0 += NW) {
+            const int blk = b0 + warp;
+            const int bx = (blk % 4) * kBlockW, by = (blk / 4) * kBlockH;
+            const bool blk_ok = blk < NBLK && by < ny && bx < nx; // uniform per warp
+            if (single_pass && !blk_ok) continue; // (chunked mode keeps every warp in the CTA-wide list builds)
+            const int cx = bx + (lane % kBlockW), cy = by + (lane / kBlockW); // my su in the tile
+            const int tcx = cx + HW, tcy = cy + HH;                             // ... in region coordinates
+            const bool in_grid = blk_ok && cx < nx && cy < ny;
+            const long long cell = in_grid ? cell_index(g, x0 + cx, y0 + cy) : -1;
+            float4* rec = reinterpret_cast<float4*>(a.dyn + (cell < 0 ? 0 : cell) * 24);
+            // events that can reach the block lie in a contiguous range of the x-sorted list
+            int e_lo = 0, e_hi = n_events;
+            if (single_pass) {
+                e_lo = colstart[max(bx, 0)];
+                e_hi = colstart[min(bx + kBlockW + 2 * HW, RW)];
+                if (e_lo == e_hi) continue; // uniform
+            }
+
+#pragma unroll 1
+            for (int kind = 0; kind < kKinds; ++kind) {
+                const KindTableDev kt = a.t.k[kind];
+                int tbase = 0;
+                for (int k = 0; k < kind; ++k) tbase += a.t.k[k].fw * a.t.k[k].fh;
+                const double* kmag = a.tab_smem ? tab_mag + tbase : kt.mag;
+                const uint32_t* kinfo = a.tab_smem ? tab_info + tbase : kt.info;
+#pragma unroll 1
+                for (int sg = 0; sg < NG; ++sg) {
+                    unsigned long long dirty = 0ull;
+                    if (single_pass) {
+                        if (in_grid) walk(e_lo, e_hi, kind, sg, kt, kmag, kinfo, tcx, tcy, by + HH, dirty);
+                    } else { // chunked region: the list is rebuilt per (kind, group)
+                        for (int c0 = 0; c0 < RW; c0 += cols_per_pass) {
+                            const int n = build_list(c0, min(RW, c0 + cols_per_pass));
+                            if (n > 0 && in_grid) walk(0, n, kind, sg, kt, kmag, kinfo, tcx, tcy, by + HH, dirty);
+                            __syncthreads();
+                        }
                     }
-                }
-                if (dirty == 0ull) continue;
-                // one 32-byte sector (or the SG-float part of it) per (su, kind)
-                float r[SG];
-                float* base = reinterpret_cast<float*>(rec) + kind * kSects + sg * SG;
-                if constexpr (SG == 2) {
-                    const float2 v = *reinterpret_cast<const float2*>(base);
-                    r[0] = v.x; r[1] = v.y;
-                } else {
+                    if (dirty == 0ull) continue;
+                    // one 32-byte sector (or the SG-float part of it) per (su, kind)
+                    float r[SG];
+                    float* base = reinterpret_cast<float*>(rec) + kind * kSects + sg * SG;
+                    if constexpr (SG == 2) {
+                        const float2 v = *reinterpret_cast<const float2*>(base);
+                        r[0] = v.x; r[1] = v.y;
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < SG / 4; ++q) {
-                        const float4 v = reinterpret_cast<const float4*>(base)[q];
-                        r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+                        for (int q = 0; q < SG / 4; ++q) {
+                            const float4 v = reinterpret_cast<const float4*>(base)[q];
+                            r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+                        }
                     }
-                }
-                fold(dirty, r);
-                if constexpr (SG == 2) {
-                    *reinterpret_cast<float2*>(base) = make_float2(r[0], r[1]);
-                } else {
+                    fold(dirty, r);
+                    if constexpr (SG == 2) {
+                        *reinterpret_cast<float2*>(base) = make_float2(r[0], r[1]);
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < SG / 4; ++q)
-                        reinterpret_cast<float4*>(base)[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                        for (int q = 0; q < SG / 4; ++q)
+                            reinterpret_cast<float4*>(base)[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    }
                 }
             }
         }
+    }
+}
+
+template <int K, int SG, int ROWS, int NT, int MODE>
+__global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    if (MODE != kModeDense && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
+    if (a.ctl->error_code != 0) return;
+    const Smem sm = carve(smem_raw, a);
+    if (a.tab_smem) { // contributor tables: one copy per CTA
+        int base = 0;
+        for (int k = 0; k < kKinds; ++k) {
+            const int n = a.t.k[k].fw * a.t.k[k].fh;
+            for (int i = tid; i < n; i += NT) {
+                sm.tab_mag[base + i] = a.t.k[k].mag[i];
+                sm.tab_info[base + i] = a.t.k[k].info[i];
+            }
+            base += n;
+        }
+    }
+    __syncthreads();
+    if constexpr (MODE == kModeDense) { // persistent over the tiles the scatter kernel declined
+        const int n = a.ctl->dense_count;
+        for (int i = blockIdx.x; i < n; i += gridDim.x) {
+            process_tile<K, SG, ROWS, NT, MODE>(a, sm, a.dense_list[i]);
+            __syncthreads();
+        }
+    } else {
+        process_tile<K, SG, ROWS, NT, MODE>(a, sm, blockIdx.x);
     }
 }
 
@@ -426,12 +513,9 @@ struct K5Shape {
     int cap, rw_max, tab_smem, part_doubles;
 };
 
-// shared-memory bytes of the event-centric scatter: 256 su x 24 addresses x (double + count byte) + masks
-constexpr int kScatterBytes = 256 * 24 * 8 + 256 * 24 + 256 * 4;
-
-template <int K, int SG, int ROWS>
+template <int K, int SG, int ROWS, int NT, int MODE>
 K5Shape k5_shape(const TablesDev& t) {
-    constexpr int MH = kNW * ROWS;
+    constexpr int MH = kBlockH * ROWS;
     K5Shape s;
     s.rw_max = kTileW + 2 * t.max_hw;
     const int rh_max = MH + 2 * t.max_hh;
@@ -440,11 +524,9 @@ K5Shape k5_shape(const TablesDev& t) {
     if (s.cap < rh_max) s.cap = rh_max; // at least one column per pass
     s.cap = (s.cap + 31) & ~31;
     s.tab_smem = t.total_entries <= kTabSmemMax;
-    size_t b = 0;
-    size_t part_bytes = sizeof(double) * SG * K * kNT;
-    if (ROWS == 2 && s.tab_smem && part_bytes < (size_t)kScatterBytes) part_bytes = kScatterBytes;
-    s.part_doubles = (int)(part_bytes / sizeof(double));
-    b += part_bytes;
+    const size_t part_bytes = MODE == kModeScatter ? (size_t)kScatterBytes : sizeof(double) * SG * K * NT;
+    s.part_doubles = (int)((part_bytes + 7) / 8);
+    size_t b = (size_t)s.part_doubles * 8;
     b += sizeof(uint2) * (size_t)s.cap;
     if (s.tab_smem) b += sizeof(double) * t.total_entries + sizeof(uint32_t) * ((t.total_entries + 1) & ~1);
     b += sizeof(int) * (size_t)((s.rw_max + 2 + 1) & ~1);
@@ -453,16 +535,17 @@ K5Shape k5_shape(const TablesDev& t) {
     return s;
 }
 
-template <int K, int SG, int ROWS>
-cudaError_t launch_variant(cudaStream_t stream, const K5Launch& l) {
-    constexpr int MH = kNW * ROWS;
-    const K5Shape sh = k5_shape<K, SG, ROWS>(l.t);
+template <int K, int SG, int ROWS, int NT, int MODE>
+cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
+    constexpr int MH = kBlockH * ROWS;
+    const K5Shape sh = k5_shape<K, SG, ROWS, NT, MODE>(l.t);
     K5Args a;
     a.g = l.g;
     a.t = l.t;
     a.dyn = l.dyn;
     a.ev = l.ev;
     a.ctl = l.ctl;
+    a.dense_list = l.dense_list;
     a.tiles_x = (l.g.W + kTileW - 1) / kTileW;
     a.advance_tick = l.advance_tick;
     a.cap = sh.cap;
@@ -471,62 +554,74 @@ cudaError_t launch_variant(cudaStream_t stream, const K5Launch& l) {
     a.part_doubles = sh.part_doubles;
     a.ev_max = l.ev_max;
     const int tiles_y = (l.g.rows + MH - 1) / MH;
-    const long long blocks = (long long)a.tiles_x * tiles_y;
-    k5_writeback_kernel<K, SG, ROWS><<<(unsigned)blocks, kNT, sh.smem, stream>>>(a);
+    long long blocks = (long long)a.tiles_x * tiles_y;
+    if (MODE == kModeDense && blocks > l.persistent_ctas) blocks = l.persistent_ctas;
+    k5_writeback_kernel<K, SG, ROWS, NT, MODE><<<(unsigned)blocks, NT, sh.smem, stream>>>(a);
     return cudaGetLastError();
 }
 
 // The attribute is per-function process state shared by every engine: only ever raise it.
-template <int K, int SG, int ROWS>
-cudaError_t prepare_variant(const TablesDev& t) {
+template <int K, int SG, int ROWS, int NT, int MODE>
+cudaError_t prepare_one(const TablesDev& t) {
     static size_t granted = 0;
-    const size_t want = k5_shape<K, SG, ROWS>(t).smem;
+    const size_t want = k5_shape<K, SG, ROWS, NT, MODE>(t).smem;
     if (want <= granted) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(k5_writeback_kernel<K, SG, ROWS>,
+    const cudaError_t e = cudaFuncSetAttribute(k5_writeback_kernel<K, SG, ROWS, NT, MODE>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
     if (e == cudaSuccess) granted = want;
     return e;
 }
 
-// Small fields (whole region staged at once): macro-tiles of 8 rows (two per warp).  Large fields: 4-row tiles
-// with the region staged in column chunks.
-bool small_region(const TablesDev& t) {
-    return (kTileW + 2 * t.max_hw) * (kNW * 2 + 2 * t.max_hh) <= kChunkCells;
+// Small fields (the whole 32 x 8 tile region is staged at once, tables in shared memory): scatter
+// + dense gather.  Otherwise 32 x 4 tiles, gather only, chunked staging.
+bool two_kernel_path(const TablesDev& t) {
+    return (kTileW + 2 * t.max_hw) * (kBlockH * 2 + 2 * t.max_hh) <= kChunkCells && t.total_entries <= kTabSmemMax;
+}
+
+template <int K, int SG>
+cudaError_t prepare_k(const TablesDev& t) {
+    cudaError_t e = prepare_one<K, SG, 2, 256, kModeScatter>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 2, 128, kModeDense>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 2, 128, kModeAll>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 1, 128, kModeAll>(t);
+    return e;
+}
+
+template <int K, int SG>
+cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
+    if (!two_kernel_path(l.t)) return launch_one<K, SG, 1, 128, kModeAll>(s, l);
+    if (l.ev_max <= 0 || l.dense_list == nullptr) return launch_one<K, SG, 2, 128, kModeAll>(s, l);
+    const cudaError_t e = launch_one<K, SG, 2, 256, kModeScatter>(s, l);
+    if (e != cudaSuccess) return e;
+    return launch_one<K, SG, 2, 128, kModeDense>(s, l);
 }
 
 } // namespace
 
-// Dispatch on (K, region size).  SG is bounded by SG * K <= 64.
-#define SFC_K5_DISPATCH(FN, ...)                                                          \
-    do {                                                                                  \
-        const bool small = small_region(tabs);                                            \
-        switch (chunk_k) {                                                                \
-            case 2: return small ? FN<2, 8, 2>(__VA_ARGS__) : FN<2, 8, 1>(__VA_ARGS__);   \
-            case 4: return small ? FN<4, 8, 2>(__VA_ARGS__) : FN<4, 8, 1>(__VA_ARGS__);   \
-            case 8: return small ? FN<8, 8, 2>(__VA_ARGS__) : FN<8, 8, 1>(__VA_ARGS__);   \
-            case 16: return small ? FN<16, 4, 2>(__VA_ARGS__) : FN<16, 4, 1>(__VA_ARGS__); \
-            default: return cudaErrorInvalidValue;                                        \
-        }                                                                                 \
-    } while (0)
-
-// Raises the dynamic shared-memory limit of the variant the engine will launch; done once at
+// Raises the dynamic shared-memory limits of the variants the engine may launch; done once at
 // engine construction so no attribute call lands inside a CUDA-graph capture.
-cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& tabs) { SFC_K5_DISPATCH(prepare_variant, tabs); }
-
-cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& l) {
-    const int chunk_k = l.chunk_k;
-    const TablesDev& tabs = l.t;
-    SFC_K5_DISPATCH(launch_variant, s, l);
-}
-
-size_t k5_smem_bytes(int chunk_k, const TablesDev& tabs) {
-    const bool small = small_region(tabs);
+cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t) {
     switch (chunk_k) {
-        case 2: return small ? k5_shape<2, 8, 2>(tabs).smem : k5_shape<2, 8, 1>(tabs).smem;
-        case 4: return small ? k5_shape<4, 8, 2>(tabs).smem : k5_shape<4, 8, 1>(tabs).smem;
-        case 8: return small ? k5_shape<8, 8, 2>(tabs).smem : k5_shape<8, 8, 1>(tabs).smem;
-        default: return small ? k5_shape<16, 4, 2>(tabs).smem : k5_shape<16, 4, 1>(tabs).smem;
+        case 2: return prepare_k<2, 8>(t);
+        case 4: return prepare_k<4, 8>(t);
+        case 8: return prepare_k<8, 8>(t);
+        case 16: return prepare_k<16, 4>(t);
+        default: return cudaErrorInvalidValue;
     }
 }
+
+cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& l) {
+    switch (l.chunk_k) {
+        case 2: return launch_k<2, 8>(s, l);
+        case 4: return launch_k<4, 8>(s, l);
+        case 8: return launch_k<8, 8>(s, l);
+        case 16: return launch_k<16, 4>(s, l);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// Number of kernels one launch_k5_writeback enqueues, and the tile count the dense list must hold.
+int k5_kernels_per_launch(const TablesDev& t, int ev_max) { return two_kernel_path(t) && ev_max > 0 ? 2 : 1; }
+long long k5_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + 7) / 8); }
 
 } // namespace sfc

@@ -193,6 +193,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
                unsigned long long* __restrict__ moved_counts, DebugArrays dbg) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool moved = false;
+    if (i == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
     if (i < p.n && ctl->error_code == 0) {
         const int d = p.dir[i];
         const int2 c = p.center[i];
