@@ -58,7 +58,7 @@ typedef struct sfc_config {
     /* Row slab owned by this engine (multi-GPU): rows [slab_row0, slab_row0 + slab_rows).
      * slab_rows = 0 means the whole grid. */
     int32_t slab_row0, slab_rows;
-    int32_t reserved;
+    int32_t slab_halo;             /* resident rows beyond each slab edge (see sfc_slab_halo_rows) */
 } sfc_config;
 
 /* Merged contributor table of one dynamic kind, replacing Engine::build_gather_tables
@@ -178,6 +178,28 @@ int sfc_reset_dynamic_images(sfc_engine* e);
  * floats) when that is not NULL — and copies the result to `out` ([H*W*8], may be NULL). */
 int sfc_rasterize_static(sfc_engine* e, int32_t n_tables, const sfc_kind_table* tables, int64_t n_anchors,
                          const sfc_anchor* anchors, const float* base, float* out);
+
+/* ---- Row slabs across GPUs (no counterpart in the reference, which is single address space;
+ * SURVEY.md 8e).  An engine created with sfc_config.slab_rows < height owns rows
+ * [slab_row0, slab_row0 + slab_rows) and keeps slab_halo more rows resident on each side.
+ * sfc_upload takes the WHOLE-grid host state and copies the slab's part; sfc_download writes back
+ * only the rows and pedestrians the slab owns.  One tick = three device steps with a halo exchange
+ * after step 0 (kind 0) and after step 1 (kinds 1, 2, 3):
+ *   kind 0 decisions of boundary pedestrians   kind 1 positions of boundary pedestrians
+ *   kind 2 occupancy rows                      kind 3 event-map rows
+ * My `edge` (0 = low-y, 1 = high-y) send buffer goes to the ring neighbour's facing (1 - edge)
+ * receive buffer.  sfc_slab_buffer returns device pointers so the transport (peer copy, NCCL) is
+ * the caller's choice. */
+int sfc_slab_halo_rows(int field_half_h, int ped_half_h, int density_radius_if_regulated);
+int sfc_slab_begin(sfc_engine* e, int64_t ticks);
+int sfc_slab_step(sfc_engine* e, int step);
+int sfc_slab_buffer(sfc_engine* e, int kind, int edge, int recv, void** ptr, size_t* bytes);
+/* Synchronises, reports a device-side error, returns TickMetrics::moved of ticks [first, first+ticks)
+ * counted since sfc_slab_begin (this slab's movers only). */
+int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* moved);
+/* Single-process driver: runs `ticks` ticks over n slab engines (ordered by slab_row0), exchanging
+ * halos with peer copies.  metrics: NULL or [ticks] (moved summed over slabs). */
+int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* metrics);
 
 /* Counters for bench.py: kernels launched by this engine since creation, bytes copied. */
 typedef struct sfc_counters {

@@ -43,6 +43,12 @@ struct sfc_engine {
     cudaGraphExec_t graph = nullptr;
     bool graph_valid = false;
 
+    // row-slab mode (multi-GPU): halo exchange buffers, [edge 0 = low-y, 1 = high-y][kind 0 = decisions, 1 = positions]
+    SlabDev slab{};
+    HaloRecord* halo_send[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    HaloRecord* halo_recv[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    int halo_capacity = 0; // records per buffer, header included
+    int ped_half_h = 0;    // largest pedestrian half-height of the uploaded population
     int* dense_list = nullptr; // k-5 tile ids handed from the scatter to the gather kernel
     int persistent_ctas = 148 * 3;
     int k5_launches = 1;       // kernels per k-5 phase
@@ -156,6 +162,39 @@ int ensure_stage(sfc_engine* e) {
     return SFC_OK;
 }
 
+// Contiguous runs of resident rows: (first global row, first local row, row count).  The whole-grid
+// engine has one; a slab has its owned rows plus up to two halo runs per side (periodic wrap) or
+// fewer (closed boundary: rows beyond the grid do not exist and keep their "empty" initial value).
+struct RowSeg {
+    int global_row, local_row, rows;
+};
+
+std::vector<RowSeg> row_segments(const sfc_engine* e, bool owned_only) {
+    std::vector<RowSeg> out;
+    const GridDev& g = e->g;
+    const int first = owned_only ? 0 : -g.halo, last = owned_only ? g.rows : g.rows + g.halo; // slab-relative
+    int run_start = 0, run_global = 0, run_len = 0;
+    for (int r = first; r < last; ++r) {
+        int y = g.row0 + r;
+        bool exists = true;
+        if (g.closed) exists = y >= 0 && y < g.H;
+        else y = emod(y, g.H);
+        if (exists && run_len > 0 && y == run_global + run_len) {
+            ++run_len;
+            continue;
+        }
+        if (run_len > 0) out.push_back(RowSeg{run_global, run_start + g.halo, run_len});
+        run_len = 0;
+        if (exists) {
+            run_start = r;
+            run_global = y;
+            run_len = 1;
+        }
+    }
+    if (run_len > 0) out.push_back(RowSeg{run_global, run_start + g.halo, run_len});
+    return out;
+}
+
 int ensure_debug(sfc_engine* e) {
     if (e->dbg.enroll_ids) return SFC_OK;
     const long long c = e->cells;
@@ -216,9 +255,9 @@ K5Launch k5_args(sfc_engine* e, int advance) {
 
 int enqueue_tick_kernels(sfc_engine* e) {
     const DebugArrays none{};
-    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
-    SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
-    SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none));
+    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
+    SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
+    SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
     SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
     return SFC_OK;
 }
@@ -299,7 +338,14 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->g.row0 = cfg->slab_rows > 0 ? cfg->slab_row0 : 0;
     e->g.rows = cfg->slab_rows > 0 ? cfg->slab_rows : cfg->height;
     e->g.halo = 0;
-    if (e->g.rows != cfg->height) return bail(fail(e, SFC_E_CONFIG, "slab_rows: partial slabs are not enabled in this build"));
+    if (e->g.rows != cfg->height) { // a proper row slab: resident rows = owned + halo on both sides
+        e->slab.active = 1;
+        e->g.halo = cfg->slab_halo;
+        if (e->g.row0 < 0 || e->g.rows < 1 || e->g.row0 + e->g.rows > cfg->height)
+            return bail(fail(e, SFC_E_CONFIG, "slab_rows: slab does not lie inside the grid"));
+        if (e->g.halo < 1 || e->g.halo > e->g.rows || e->g.rows + 2 * e->g.halo > cfg->height)
+            return bail(fail(e, SFC_E_CONFIG, "slab_halo: need 1 <= halo <= slab_rows and slab_rows + 2*halo <= height"));
+    }
     e->dp.w_static = cfg->weight_static;
     e->dp.w_kind[0] = cfg->weight_dir_attractive;
     e->dp.w_kind[1] = cfg->weight_dir_repulsive;
@@ -335,6 +381,21 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
     cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
     cu(dev_alloc(&e->dense_list, k5_tile_count(e->g)), "cudaMalloc(dense tile list)");
+    if (e->slab.active) {
+        const long long band = (long long)e->g.W * (2 * e->g.halo) + 1;
+        e->halo_capacity = (int)std::min<long long>(band, 1 << 18);
+        for (int edge = 0; edge < 2; ++edge)
+            for (int kind = 0; kind < 2; ++kind) {
+                cu(dev_alloc(&e->halo_send[edge][kind], e->halo_capacity), "cudaMalloc(halo send)");
+                cu(dev_alloc(&e->halo_recv[edge][kind], e->halo_capacity), "cudaMalloc(halo recv)");
+                if (rc == SFC_OK) {
+                    cu(cudaMemset(e->halo_send[edge][kind], 0, sizeof(HaloRecord)), "cudaMemset");
+                    cu(cudaMemset(e->halo_recv[edge][kind], 0, sizeof(HaloRecord)), "cudaMemset");
+                }
+            }
+        e->slab.ev_capacity = 4ll * e->halo_capacity + 1024;
+        cu(dev_alloc(&e->slab.ev_written, e->slab.ev_capacity), "cudaMalloc(event written list)");
+    }
     {
         cudaDeviceProp prop{};
         if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->persistent_ctas = prop.multiProcessorCount * 3;
@@ -368,6 +429,12 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->ev);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
+    for (int edge = 0; edge < 2; ++edge)
+        for (int kind = 0; kind < 2; ++kind) {
+            cudaFree(e->halo_send[edge][kind]);
+            cudaFree(e->halo_recv[edge][kind]);
+        }
+    cudaFree(e->slab.ev_written);
     cudaFree(e->moved_counts);
     cudaFree(e->stage);
     cudaFree(e->dbg.enroll_ids);
@@ -404,24 +471,31 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
     // pedestrian attributes: pack on the host (cheap, one pass), copy once
     std::vector<int2> gate((size_t)P);
     std::vector<uint32_t> attr((size_t)P);
+    int max_hh = 0;
     for (long long i = 0; i < P; ++i) {
         const int hw = (v->foot_w[i] - 1) / 2, hh = (v->foot_h[i] - 1) / 2;
         if (hw > kMaxHalfExtent || hh > kMaxHalfExtent || hw < 0 || hh < 0)
             return fail(e, SFC_E_CONFIG, "footprint: pedestrian footprint exceeds the device limit (4095)");
+        max_hh = std::max(max_hh, hh);
         gate[(size_t)i] = make_int2(v->walk_period[i], v->walk_phase[i]);
         attr[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
     }
-    SFC_CUDA(cudaMemcpyAsync(e->occ, v->occupancy, sizeof(int) * (size_t)C, cudaMemcpyHostToDevice, e->stream));
-    SFC_CUDA(cudaMemcpyAsync(e->stat, v->static_image, sizeof(float) * (size_t)C * kSects, cudaMemcpyHostToDevice, e->stream));
-    e->counters.h2d_bytes += (int64_t)(sizeof(int) * C + sizeof(float) * C * kSects);
-    for (int k = 0; k < kKinds; ++k) {
-        for (long long c0 = 0; c0 < C; c0 += e->stage_cells) {
-            const long long n = std::min(e->stage_cells, C - c0);
-            SFC_CUDA(cudaMemcpyAsync(e->stage, v->dyn_images[k] + c0 * kSects, sizeof(float) * (size_t)n * kSects,
-                                     cudaMemcpyHostToDevice, e->stream));
-            SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, c0, n));
-            e->counters.kernel_launches += 1;
-            e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
+    const long long W = e->g.W;
+    for (const RowSeg& seg : row_segments(e, false)) { // the host arrays cover the whole grid
+        const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
+        SFC_CUDA(cudaMemcpyAsync(e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemcpyAsync(e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects,
+                                 cudaMemcpyHostToDevice, e->stream));
+        e->counters.h2d_bytes += (int64_t)(sizeof(int) * n_seg + sizeof(float) * n_seg * kSects);
+        for (int k = 0; k < kKinds; ++k) {
+            for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
+                const long long n = std::min(e->stage_cells, n_seg - c0);
+                SFC_CUDA(cudaMemcpyAsync(e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects,
+                                         cudaMemcpyHostToDevice, e->stream));
+                SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, dc + c0, n));
+                e->counters.kernel_launches += 1;
+                e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
+            }
         }
     }
     if (P > 0) {
@@ -433,6 +507,14 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         SFC_CUDA(cudaMemsetAsync(e->peds.won, 0, (size_t)P, e->stream));
         SFC_CUDA(cudaMemsetAsync(e->peds.score, 0, sizeof(double) * (size_t)P, e->stream));
         e->counters.h2d_bytes += (int64_t)((sizeof(int2) * 2 + sizeof(uint32_t)) * P);
+    }
+    if (e->slab.active) {
+        e->ped_half_h = max_hh;
+        e->slab.reach = max_hh + 1;
+        const int need = 4 * (max_hh + 1) + (e->dp.regulated ? e->dp.density_radius : 0);
+        if (e->g.halo < need || e->g.halo < e->tabs.max_hh)
+            return fail(e, SFC_E_CONFIG, "slab_halo: too shallow for this population (need max(field half-height, "
+                                         "4*(pedestrian half-height+1) + density radius) rows)");
     }
     SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
     Ctl h{};
@@ -448,31 +530,47 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
 int sfc_download(sfc_engine* e, sfc_state_view* v) {
     if (!e->uploaded) return fail(e, SFC_E_STATE, "download before upload");
     SFC_CUDA(cudaSetDevice(e->device));
-    const long long C = e->cells, P = e->peds.n;
+    const long long P = e->peds.n;
     int rc = ensure_stage(e);
     if (rc != SFC_OK) return rc;
-    if (v->occupancy) {
-        SFC_CUDA(cudaMemcpyAsync(v->occupancy, e->occ, sizeof(int) * (size_t)C, cudaMemcpyDeviceToHost, e->stream));
-        e->counters.d2h_bytes += (int64_t)(sizeof(int) * C);
-    }
-    for (int k = 0; k < kKinds; ++k) {
-        if (!v->dyn_images[k]) continue;
-        for (long long c0 = 0; c0 < C; c0 += e->stage_cells) {
-            const long long n = std::min(e->stage_cells, C - c0);
-            SFC_CUDA(launch_deinterleave(e->stream, e->dyn, e->stage, k, c0, n));
-            SFC_CUDA(cudaMemcpyAsync(v->dyn_images[k] + c0 * kSects, e->stage, sizeof(float) * (size_t)n * kSects,
+    const long long W = e->g.W;
+    for (const RowSeg& seg : row_segments(e, true)) { // only the rows this engine owns are authoritative
+        const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
+        if (v->occupancy) {
+            SFC_CUDA(cudaMemcpyAsync(v->occupancy + hc, e->occ + dc, sizeof(int) * (size_t)n_seg, cudaMemcpyDeviceToHost, e->stream));
+            e->counters.d2h_bytes += (int64_t)(sizeof(int) * n_seg);
+        }
+        for (int k = 0; k < kKinds; ++k) {
+            if (!v->dyn_images[k]) continue;
+            for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
+                const long long n = std::min(e->stage_cells, n_seg - c0);
+                SFC_CUDA(launch_deinterleave(e->stream, e->dyn, e->stage, k, dc + c0, n));
+                SFC_CUDA(cudaMemcpyAsync(v->dyn_images[k] + (hc + c0) * kSects, e->stage, sizeof(float) * (size_t)n * kSects,
+                                         cudaMemcpyDeviceToHost, e->stream));
+                SFC_CUDA(cudaStreamSynchronize(e->stream)); // staging buffer is reused by the next chunk
+                e->counters.kernel_launches += 1;
+                e->counters.d2h_bytes += (int64_t)(sizeof(float) * n * kSects);
+            }
+        }
+        if (v->static_image) {
+            SFC_CUDA(cudaMemcpyAsync(v->static_image + hc * kSects, e->stat + dc * kSects, sizeof(float) * (size_t)n_seg * kSects,
                                      cudaMemcpyDeviceToHost, e->stream));
-            SFC_CUDA(cudaStreamSynchronize(e->stream)); // staging buffer is reused by the next chunk
-            e->counters.kernel_launches += 1;
-            e->counters.d2h_bytes += (int64_t)(sizeof(float) * n * kSects);
+            e->counters.d2h_bytes += (int64_t)(sizeof(float) * n_seg * kSects);
         }
     }
-    if (v->static_image) {
-        SFC_CUDA(cudaMemcpyAsync(v->static_image, e->stat, sizeof(float) * (size_t)C * kSects, cudaMemcpyDeviceToHost, e->stream));
-        e->counters.d2h_bytes += (int64_t)(sizeof(float) * C * kSects);
-    }
     if (v->center_xy && P > 0) {
-        SFC_CUDA(cudaMemcpyAsync(v->center_xy, e->peds.center, sizeof(int2) * (size_t)P, cudaMemcpyDeviceToHost, e->stream));
+        if (!e->slab.active) {
+            SFC_CUDA(cudaMemcpyAsync(v->center_xy, e->peds.center, sizeof(int2) * (size_t)P, cudaMemcpyDeviceToHost, e->stream));
+        } else { // a slab only vouches for the pedestrians whose centre lies in its rows
+            std::vector<int2> mine((size_t)P);
+            SFC_CUDA(cudaMemcpyAsync(mine.data(), e->peds.center, sizeof(int2) * (size_t)P, cudaMemcpyDeviceToHost, e->stream));
+            SFC_CUDA(cudaStreamSynchronize(e->stream));
+            for (long long i = 0; i < P; ++i) {
+                if (!row_owned(e->g, mine[(size_t)i].y)) continue;
+                v->center_xy[2 * i] = mine[(size_t)i].x;
+                v->center_xy[2 * i + 1] = mine[(size_t)i].y;
+            }
+        }
         e->counters.d2h_bytes += (int64_t)(sizeof(int2) * P);
     }
     rc = check_device_error(e); // also refreshes e->tick
@@ -509,11 +607,11 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
             SFC_CUDA(cudaEventRecord(ev[0], e->stream));
             // k-1 has no device work: its slot reports zero
             SFC_CUDA(cudaEventRecord(ev[1], e->stream));
-            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
             SFC_CUDA(cudaEventRecord(ev[2], e->stream));
-            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
             SFC_CUDA(cudaEventRecord(ev[3], e->stream));
-            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
             SFC_CUDA(cudaEventRecord(ev[4], e->stream));
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
             if (t == ticks - 1) SFC_CUDA(cudaEventRecord(evs[(size_t)ticks * 5], e->stream));
@@ -576,17 +674,17 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
             break;
         }
         case 2:
-            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
             SFC_CUDA(launch_dbg_enroll(e->stream, e->g, e->peds, e->dbg, e->ctl));
             e->counters.kernel_launches += 2;
             break;
         case 3:
-            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp));
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
             SFC_CUDA(launch_dbg_vote(e->stream, e->dbg, e->dp.fault_invert));
             e->counters.kernel_launches += 2;
             break;
         case 4:
-            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, e->dbg));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, e->dbg, e->slab));
             e->counters.kernel_launches += 1;
             break;
         case 5:
@@ -643,7 +741,7 @@ int sfc_decide(sfc_engine* e, int64_t ped, int32_t* direction, double* score) {
     if (!e->uploaded) return fail(e, SFC_E_STATE, "decide before upload");
     if (ped < 0 || ped >= e->peds.n) return fail(e, SFC_E_STATE, "pedestrian index out of range");
     SFC_CUDA(cudaSetDevice(e->device));
-    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp));
+    SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
     e->counters.kernel_launches += 1;
     int8_t d = -1;
     SFC_CUDA(cudaMemcpyAsync(&d, e->peds.dir + ped, 1, cudaMemcpyDeviceToHost, e->stream));
@@ -713,6 +811,190 @@ int sfc_rasterize_static(sfc_engine* e, int32_t n_tables, const sfc_kind_table* 
     for (size_t i = first_alloc; i < e->table_allocs.size(); ++i) cudaFree(e->table_allocs[i]);
     e->table_allocs.resize(first_alloc);
     return rc;
+}
+
+// ---- row slabs (multi-GPU) -------------------------------------------------------------------
+
+int sfc_slab_halo_rows(int field_half_h, int ped_half_h, int density_radius_if_regulated) {
+    return std::max(field_half_h, 4 * (ped_half_h + 1) + density_radius_if_regulated);
+}
+
+static bool slab_has_neighbour(const sfc_engine* e, int edge) {
+    if (!e->g.closed) return true;
+    return edge == 0 ? e->g.row0 > 0 : e->g.row0 + e->g.rows < e->g.H;
+}
+
+int sfc_slab_step(sfc_engine* e, int step) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "slab step before upload");
+    if (!e->slab.active) return fail(e, SFC_E_STATE, "slab step on a whole-grid engine");
+    SFC_CUDA(cudaSetDevice(e->device));
+    const DebugArrays none{};
+    const int depth = std::min(e->g.halo + e->ped_half_h, e->g.rows);
+    switch (step) {
+        case 0: // retire last tick's events, decide, publish the decisions of my boundary pedestrians
+            SFC_CUDA(launch_clear_events(e->stream, e->ev, e->ctl, e->slab));
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
+            for (int edge = 0; edge < 2; ++edge)
+                SFC_CUDA(launch_halo_pack(e->stream, e->g, e->peds, e->ctl, edge, 0, depth, e->halo_send[edge][0], e->halo_capacity));
+            e->counters.kernel_launches += 7;
+            break;
+        case 1: // adopt the neighbours' decisions, vote, move, publish the positions of my boundary pedestrians
+            for (int edge = 0; edge < 2; ++edge)
+                if (slab_has_neighbour(e, edge))
+                    SFC_CUDA(launch_halo_unpack(e->stream, e->peds, e->ctl, 0, e->halo_recv[edge][0], e->halo_capacity));
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
+            for (int edge = 0; edge < 2; ++edge)
+                SFC_CUDA(launch_halo_pack(e->stream, e->g, e->peds, e->ctl, edge, 1, depth, e->halo_send[edge][1], e->halo_capacity));
+            e->counters.kernel_launches += 8;
+            break;
+        case 2: { // adopt the neighbours' positions (their rows of occupancy / events arrived as plain copies), write back
+            for (int edge = 0; edge < 2; ++edge)
+                if (slab_has_neighbour(e, edge))
+                    SFC_CUDA(launch_halo_unpack(e->stream, e->peds, e->ctl, 1, e->halo_recv[edge][1], e->halo_capacity));
+            SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
+            e->counters.kernel_launches += 2 + e->k5_launches;
+            const long long interval = e->cfg.rebuild_interval;
+            if (interval > 0 && (e->tick + 1) % interval == 0) {
+                const int rc = enqueue_rebuild(e);
+                if (rc != SFC_OK) return rc;
+            }
+            e->tick += 1; // host shadow; the device counter advanced inside k-5
+            break;
+        }
+        default: return fail(e, SFC_E_STATE, "slab step must be 0, 1 or 2");
+    }
+    return SFC_OK;
+}
+
+int sfc_slab_buffer(sfc_engine* e, int kind, int edge, int recv, void** ptr, size_t* bytes) {
+    if (!e->slab.active || edge < 0 || edge > 1 || kind < 0 || kind > 3) return fail(e, SFC_E_STATE, "no such halo buffer");
+    const long long W = e->g.W, halo = e->g.halo, rows = e->g.rows;
+    if (kind < 2) {
+        *ptr = recv ? e->halo_recv[edge][kind] : e->halo_send[edge][kind];
+        *bytes = sizeof(HaloRecord) * (size_t)e->halo_capacity;
+        return SFC_OK;
+    }
+    // dense rows: send = my first / last `halo` owned rows, receive = the halo rows beyond that edge
+    const long long send_row = edge == 0 ? halo : rows;           // local row index (owned rows start at `halo`)
+    const long long recv_row = edge == 0 ? 0 : halo + rows;
+    const long long row = recv ? recv_row : send_row;
+    if (kind == 2) {
+        *ptr = e->occ + row * W;
+        *bytes = sizeof(int) * (size_t)(halo * W);
+    } else {
+        *ptr = e->ev + 2 * row * W;
+        *bytes = (size_t)(2 * halo * W);
+    }
+    return SFC_OK;
+}
+
+int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* moved) {
+    SFC_CUDA(cudaSetDevice(e->device));
+    std::vector<unsigned long long> m((size_t)std::max<int64_t>(ticks, 0));
+    if (ticks > 0 && moved) {
+        SFC_CUDA(cudaMemcpyAsync(m.data(), e->moved_counts + first_tick, sizeof(unsigned long long) * (size_t)ticks,
+                                 cudaMemcpyDeviceToHost, e->stream));
+    }
+    const int rc = check_device_error(e);
+    if (moved)
+        for (int64_t t = 0; t < ticks; ++t) moved[t] = (int64_t)m[(size_t)t];
+    return rc;
+}
+
+int sfc_slab_begin(sfc_engine* e, int64_t ticks) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "slab run before upload");
+    SFC_CUDA(cudaSetDevice(e->device));
+    const int rc = ensure_moved(e, ticks);
+    if (rc != SFC_OK) return rc;
+    SFC_CUDA(cudaMemsetAsync(e->moved_counts, 0, sizeof(unsigned long long) * (size_t)std::max<int64_t>(ticks, 1), e->stream));
+    const long long base = e->tick;
+    SFC_CUDA(cudaMemcpyAsync(&e->ctl->run_base, &base, sizeof(long long), cudaMemcpyHostToDevice, e->stream));
+    SFC_CUDA(cudaStreamSynchronize(e->stream));
+    return SFC_OK;
+}
+
+// Single-process driver for N slab engines (same or different devices): the halo exchange is a set
+// of peer copies between the engines' buffers.  The multi-process path (one rank per GPU,
+// torch.distributed / NCCL send-recv on the same buffers) lives in paper_1803_04782_b200/slabs.py.
+int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* metrics) {
+    if (n < 1) return SFC_E_STATE;
+    sfc_engine* e0 = engines[0];
+    if (ticks <= 0) return SFC_OK;
+    const long long base = e0->tick;
+    for (int i = 0; i < n; ++i) {
+        const int rc = sfc_slab_begin(engines[i], ticks);
+        if (rc != SFC_OK) return rc;
+    }
+    auto sync_all = [&]() -> cudaError_t {
+        for (int i = 0; i < n; ++i) {
+            cudaSetDevice(engines[i]->device);
+            const cudaError_t c = cudaStreamSynchronize(engines[i]->stream);
+            if (c != cudaSuccess) return c;
+        }
+        return cudaSuccess;
+    };
+    auto exchange = [&](int kind) -> int { // my edge -> the facing edge of the ring neighbour
+        for (int i = 0; i < n; ++i) {
+            sfc_engine* e = engines[i];
+            for (int edge = 0; edge < 2; ++edge) {
+                if (!slab_has_neighbour(e, edge)) continue;
+                sfc_engine* nb = engines[(i + (edge == 0 ? n - 1 : 1)) % n];
+                void *src = nullptr, *dst = nullptr;
+                size_t sb = 0, db = 0;
+                int rc = sfc_slab_buffer(e, kind, edge, 0, &src, &sb);
+                if (rc == SFC_OK) rc = sfc_slab_buffer(nb, kind, 1 - edge, 1, &dst, &db);
+                if (rc != SFC_OK || sb != db) return fail(e, SFC_E_STATE, "halo buffers of neighbouring slabs do not match");
+                const cudaError_t c = cudaMemcpyPeerAsync(dst, nb->device, src, e->device, sb, nb->stream);
+                if (c != cudaSuccess) return cuda_fail(e, c, "cudaMemcpyPeerAsync(halo)");
+            }
+        }
+        return SFC_OK;
+    };
+    for (int64_t t = 0; t < ticks; ++t) {
+        for (int step = 0; step < 3; ++step) {
+            for (int i = 0; i < n; ++i) {
+                const int rc = sfc_slab_step(engines[i], step);
+                if (rc != SFC_OK) return rc;
+            }
+            cudaError_t c = sync_all();
+            if (c != cudaSuccess) return cuda_fail(e0, c, "slab step");
+            if (step == 0) {
+                const int rc = exchange(0);
+                if (rc != SFC_OK) return rc;
+            } else if (step == 1) {
+                for (int kind = 1; kind <= 3; ++kind) {
+                    const int rc = exchange(kind);
+                    if (rc != SFC_OK) return rc;
+                }
+            }
+            c = sync_all();
+            if (c != cudaSuccess) return cuda_fail(e0, c, "halo exchange");
+        }
+    }
+    int status = SFC_OK;
+    std::vector<int64_t> moved((size_t)ticks), total((size_t)ticks, 0);
+    for (int i = 0; i < n; ++i) {
+        const int rc = sfc_slab_finish(engines[i], 0, ticks, moved.data());
+        if (rc != SFC_OK && status == SFC_OK) {
+            status = rc;
+            if (engines[i] != e0) { // surface the failing slab's diagnosis on the handle the caller inspects
+                e0->err = engines[i]->err;
+                e0->err_tick = engines[i]->err_tick;
+                e0->err_phase = engines[i]->err_phase;
+                e0->err_value = engines[i]->err_value;
+            }
+        }
+        for (int64_t t = 0; t < ticks; ++t) total[(size_t)t] += moved[(size_t)t];
+    }
+    if (metrics) {
+        for (int64_t t = 0; t < ticks; ++t) {
+            metrics[t] = sfc_tick_metrics{};
+            metrics[t].tick = base + t;
+            metrics[t].moved = total[(size_t)t];
+        }
+    }
+    return status;
 }
 
 void sfc_get_counters(const sfc_engine* e, sfc_counters* out) { *out = e->counters; }

@@ -63,6 +63,21 @@ __host__ __device__ __forceinline__ bool row_owned(const GridDev& g, int y) {
     return ly >= 0 && ly < g.rows;
 }
 
+// True when global row y lies at most `depth` rows beyond this slab's owned range (depth 0 = owned).
+__host__ __device__ __forceinline__ bool row_within(const GridDev& g, int y, int depth) {
+    int ly = y - g.row0;
+    if (!g.closed) ly = emod(ly + depth, g.H) - depth;
+    return ly >= -depth && ly < g.rows + depth;
+}
+
+// Multi-GPU row slabs: what the per-pedestrian kernels need to know beyond GridDev.
+struct SlabDev {
+    int active;               // this engine owns a proper sub-range of rows
+    int reach;                // k-3 / k-4 also run for neighbours' pedestrians this many rows beyond the edge
+    long long* ev_written;    // event-map cells written this tick (cleared at the start of the next)
+    long long ev_capacity;
+};
+
 // sect_step (fields.cpp:67-72) without a table: sect 0 = +x, counter-clockwise.
 __host__ __device__ __forceinline__ int step_dx(int sect) {
     return (sect == 0 || sect == 1 || sect == 7) ? 1 : ((sect >= 3 && sect <= 5) ? -1 : 0);
@@ -115,6 +130,8 @@ struct Ctl {
     double error_value;
     unsigned int drift_bits[kKinds]; // max |old - fresh| per kind as float bits (rebuild)
     int dense_count;         // k-5: tiles the scatter kernel handed to the gather kernel this tick
+    int ev_written_count;    // slab mode: entries of SlabDev::ev_written
+    int halo_counts[4];      // slab mode: records packed per (edge, kind): [edge*2 + kind]
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -165,11 +182,25 @@ struct K5Launch {
     int persistent_ctas; // k-5: grid of the persistent gather kernel
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
-                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp);
+                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
 cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
-                           const DecideParams& dp);
+                           const DecideParams& dp, const SlabDev& slab);
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
-                           unsigned long long* moved_counts, const DebugArrays& dbg);
+                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab);
+
+// ---- slab halo exchange (sfc_slab.cu) --------------------------------------------------------
+struct HaloRecord {   // 16 bytes: a pedestrian's decision (k-2 -> k-3) or position (k-4 -> next tick)
+    int id;
+    int a;            // decision: direction          position: x
+    double b;         // decision: score              position: y (as an exact double)
+};
+// Packs records of OWNED pedestrians whose centre lies within `depth` rows of slab edge `edge`
+// (0 = low-y edge, 1 = high-y edge) into buf[1..]; buf[0].id receives the count.  kind 0 = decisions,
+// 1 = positions.
+cudaError_t launch_halo_pack(cudaStream_t s, const GridDev& g, const PedArrays& p, Ctl* ctl, int edge, int kind,
+                             int depth, HaloRecord* buf, int capacity);
+cudaError_t launch_halo_unpack(cudaStream_t s, const PedArrays& p, Ctl* ctl, int kind, const HaloRecord* buf, int capacity);
+cudaError_t launch_clear_events(cudaStream_t s, uint8_t* ev, Ctl* ctl, const SlabDev& slab);
 cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& a);
 int k5_kernels_per_launch(const TablesDev& t, int ev_max);
 long long k5_tile_count(const GridDev& g);

@@ -61,7 +61,7 @@ __device__ __forceinline__ void cex(double& sa, int& ia, double& sb, int& ib) {
 
 __global__ void __launch_bounds__(kPedThreads)
 k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const float* __restrict__ stat,
-                 const float* __restrict__ dyn, uint8_t* __restrict__ ev, Ctl* ctl, DecideParams dp) {
+                 const float* __restrict__ dyn, uint8_t* __restrict__ ev, Ctl* ctl, DecideParams dp, SlabDev slab) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     if (ctl->error_code != 0) return;
@@ -71,7 +71,7 @@ k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const floa
 
     // Retire the previous tick's movement events of this pedestrian (the reference clears its
     // whole MovementLog in k-1, engine.cpp:335-339; here only the two touched su are reset).
-    const int md = p.moved_dir[i];
+    const int md = slab.active ? -1 : p.moved_dir[i]; // (slabs clear their event cells from a written-list instead)
     if (md >= 0) {
         const long long to = cell_index(g, c.x, c.y);
         const long long from = cell_index(g, c.x - step_dx(md), c.y - step_dy(md));
@@ -159,14 +159,14 @@ k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const floa
 }
 
 __global__ void __launch_bounds__(kPedThreads)
-k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault) {
+k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault, SlabDev slab) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     if (ctl->error_code != 0) return;
     const int d = p.dir[i];
     if (d < 0) return;
     const int2 c = p.center[i];
-    if (!row_owned(g, c.y)) return;
+    if (!row_within(g, c.y, slab.reach)) return; // owned, or a neighbour's pedestrian that can touch my rows
     const uint32_t attr = p.attr[i];
     const double my = p.score[i];
     // engine.cpp:365-386 restated per claimant: I win su c iff no other registrant of c beats
@@ -190,14 +190,14 @@ k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, in
 
 __global__ void __launch_bounds__(kPedThreads)
 k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restrict__ ev, Ctl* ctl,
-               unsigned long long* __restrict__ moved_counts, DebugArrays dbg) {
+               unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool moved = false;
     if (i == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
     if (i < p.n && ctl->error_code == 0) {
         const int d = p.dir[i];
         const int2 c = p.center[i];
-        if (d >= 0 && p.won[i] && row_owned(g, c.y)) {
+        if (d >= 0 && p.won[i] && row_within(g, c.y, slab.reach)) {
             const uint32_t attr = p.attr[i];
             const int rw = attr_half_w(attr), rh = attr_half_h(attr);
             const int ux = step_dx(d), uy = step_dy(d);
@@ -230,9 +230,16 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             p.center[i] = make_int2(nx, ny);
             const long long from = cell_index(g, c.x, c.y), to = cell_index(g, nx, ny);
             const uint8_t code = event_code(attr);
-            ev[2 * from] = code;
+            if (from >= 0) ev[2 * from] = code;
             if (to >= 0) ev[2 * to + 1] = code;
             p.moved_dir[i] = (int8_t)d;
+            if (slab.active) { // remember the event cells for next tick's clear
+                const int at = atomicAdd(&ctl->ev_written_count, 2);
+                if (at + 1 < slab.ev_capacity) {
+                    slab.ev_written[at] = from >= 0 ? 2 * from : -1;
+                    slab.ev_written[at + 1] = to >= 0 ? 2 * to + 1 : -1;
+                }
+            }
             if (dbg.moved_from) { // MovementLog as the reference shapes it (engine.cpp:412-423)
                 dbg.moved_from[from] = (int)i;
                 dbg.moved_to[to] = (int)i;
@@ -242,7 +249,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
                     dbg.to_mask[(long long)k * dbg.cells + to] = mask;
                 }
             }
-            moved = true;
+            moved = row_owned(g, c.y); // a neighbour's pedestrian is counted by its owner
         }
     }
     // TickMetrics::moved: one atomic per warp
@@ -344,20 +351,20 @@ inline unsigned blocks_for(long long n, int threads) {
 } // namespace
 
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
-                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp) {
-    k2_decide_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, stat, dyn, ev, ctl, dp);
+                             const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab) {
+    k2_decide_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, stat, dyn, ev, ctl, dp, slab);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
-                           const DecideParams& dp) {
-    k3_vote_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ctl, dp.fault_invert);
+                           const DecideParams& dp, const SlabDev& slab) {
+    k3_vote_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ctl, dp.fault_invert, slab);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
-                           unsigned long long* moved_counts, const DebugArrays& dbg) {
-    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg);
+                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab) {
+    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg, slab);
     return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 // CUDA C ABI (include/socfield_cuda.h).  No phase of the tick executes on the host.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -210,6 +211,8 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
     if (!valid_chunk_width(cfg_.chunk_k)) throw ConfigError("chunk_k", "must be 2, 4, 8, or 16");
     if (cfg_.density_radius < 0) throw ConfigError("density_radius", "must be >= 0");
     if (cfg_.workers <= 0) cfg_.workers = 1; // no host workers exist; keep the field well-formed
+    if (const char* knob = std::getenv("SFC_SLABS")) cfg_.slabs = std::atoi(knob); // test hook: force a slab group
+    if (cfg_.slabs < 1) throw ConfigError("slabs", "must be >= 1");
 
     std::array<bridge::KindTable, kDynKinds> tables;
     for (int k = 0; k < kDynKinds; ++k) {
@@ -236,7 +239,77 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
     step_caches_.assign(1, StepCache(cfg_.chunk_k));
 }
 
-Engine::~Engine() { sfc_destroy(dev_); }
+Engine::~Engine() {
+    release_slabs();
+    sfc_destroy(dev_);
+}
+
+void Engine::release_slabs() {
+    for (sfc_engine* e : slab_engines_) sfc_destroy(e);
+    slab_engines_.clear();
+}
+
+// run() over a group of row-slab engines (one per GPU when several are visible): the whole-grid
+// host state is scattered over the slabs, the C ABI's group driver steps them with a halo exchange
+// per tick, and every slab writes back the rows and pedestrians it owns.
+std::vector<TickMetrics> Engine::run_slabs(SimState& s, long ticks) {
+    int ped_half_h = 0, field_half_h = 0;
+    for (const Pedestrian& p : s.pedestrians) ped_half_h = std::max(ped_half_h, p.footprint.half_h());
+    for (const FieldSpec& f : field_templates_) field_half_h = std::max(field_half_h, f.geometry.half_h());
+    const int halo = sfc_slab_halo_rows(field_half_h, ped_half_h,
+                                        cfg_.regulation == Regulation::Linear ? cfg_.density_radius : 0);
+    if (slab_engines_.empty() || halo != slab_halo_) {
+        release_slabs();
+        const int devices = std::max(1, sfc_device_count());
+        std::array<bridge::KindTable, kDynKinds> tables;
+        for (int k = 0; k < kDynKinds; ++k) tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(field_templates_[static_cast<std::size_t>(k)]);
+        sfc_tables t{};
+        for (int k = 0; k < kDynKinds; ++k) t.kind[k] = tables[static_cast<std::size_t>(k)].view();
+        for (int i = 0; i < cfg_.slabs; ++i) {
+            EngineConfig ec = cfg_;
+            ec.device = (cfg_.device + i) % devices;
+            sfc_config c = bridge::make_config(geom_, ec);
+            c.slab_row0 = static_cast<std::int32_t>(static_cast<std::int64_t>(geom_.height) * i / cfg_.slabs);
+            c.slab_rows = static_cast<std::int32_t>(static_cast<std::int64_t>(geom_.height) * (i + 1) / cfg_.slabs) - c.slab_row0;
+            c.slab_halo = halo;
+            sfc_engine* handle = nullptr;
+            char why[512] = {0};
+            const int status = sfc_create(&c, &t, &handle, why, sizeof why);
+            if (status != SFC_OK) {
+                release_slabs();
+                bridge::throw_status(status, why, s.tick, 0);
+            }
+            slab_engines_.push_back(handle);
+        }
+        slab_halo_ = halo;
+    }
+    bridge::PedColumns cols;
+    sfc_state_view v = make_view(s, cols);
+    const auto fail_with = [&](sfc_engine* e, int status) {
+        std::int64_t tick = -1;
+        std::int32_t phase = 0;
+        sfc_error_detail(e, &tick, &phase, nullptr, nullptr, nullptr);
+        bridge::throw_status(status, sfc_last_error(e), static_cast<long>(tick), phase);
+    };
+    for (sfc_engine* e : slab_engines_) {
+        const int status = sfc_upload(e, &v);
+        if (status != SFC_OK) fail_with(e, status);
+    }
+    std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
+    const int run_status = sfc_group_run(slab_engines_.data(), static_cast<int>(slab_engines_.size()), ticks, raw.data());
+    v.static_image = nullptr;
+    for (sfc_engine* e : slab_engines_) {
+        const int status = sfc_download(e, &v);
+        if (status != SFC_OK) fail_with(e, status);
+    }
+    for (std::size_t i = 0; i < s.pedestrians.size(); ++i) s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
+    s.tick = static_cast<long>(v.tick);
+    if (run_status != SFC_OK) fail_with(slab_engines_.front(), run_status);
+    std::vector<TickMetrics> metrics;
+    metrics.reserve(raw.size());
+    for (const auto& r : raw) metrics.push_back(to_metrics(r));
+    return metrics;
+}
 
 const WritePlan& Engine::plan(DynKind kind, int orientation) const {
     const auto& plans = plans_[static_cast<std::size_t>(kind)];
@@ -354,6 +427,7 @@ std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, cons
         for (long i = 0; i < ticks; ++i) metrics.push_back(tick(s, mode, inspect));
         return metrics;
     }
+    if (cfg_.slabs > 1) return run_slabs(s, ticks);
     upload(s);
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
     const int status = sfc_run(dev_, ticks, raw.data(), 0);

@@ -1,0 +1,46 @@
+"""Row-slab decomposition (the multi-GPU path) on ONE device: N slab engines share the GPU and
+exchange halos through the same buffers and the same three-step tick protocol a multi-GPU run
+uses (peer copies here, NCCL send/recv in paper_1803_04782_b200/slabs.py).  The result must be
+bit-identical to the oracle — i.e. to the undivided grid — for every N, because every tie-break of
+the model is on pedestrian id, never on ownership."""
+import numpy as np
+import pytest
+
+from oracle import oracle, shim
+from tests import scenarios as sc
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+CASES = [
+    ("desk64", 2), ("desk64", 4), ("closed-four", 2), ("closed-ped3", 2), ("linear-regulation", 2),
+    ("linear-regulation", 3), ("wide-ragged", 3), ("field21", 2), ("ped5", 2), ("k16", 3), ("d0.9-eight-ped1", 4),
+]
+
+
+@pytest.mark.parametrize("name,slabs", CASES)
+def test_slabs_equal_undivided_grid(product_lib, monkeypatch, name, slabs):
+    monkeypatch.setenv("SFC_SLABS", str(slabs))
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for chunk in (1, 7, 22, 30):  # crosses rebuild points of every scenario that has them
+        np.testing.assert_array_equal(gpu.run(chunk), cpu.run(chunk), err_msg=f"{name} x{slabs} moved")
+        assert gpu.tick == cpu.tick
+        np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"{name} x{slabs} tick {gpu.tick} centres")
+        np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"{name} x{slabs} tick {gpu.tick} occupancy")
+        for k in range(3):
+            np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)), err_msg=f"{name} x{slabs} image {k}")
+    gpu.verify()
+
+
+def test_slab_halo_too_thin_is_a_config_error(product_lib, monkeypatch):
+    monkeypatch.setenv("SFC_SLABS", "8")  # 24 rows / 8 = 3 owned rows < halo 4
+    gpu = shim.Sim.from_scenario(product_lib, sc.SEQPAR24)
+    with pytest.raises(shim.ShimError) as e:
+        gpu.run(1)
+    assert e.value.kind == "ConfigError" and "slab_halo" in e.value.message
