@@ -184,6 +184,69 @@ def cpu_reference(w, ticks_per_step: int, steps: int, warmup: int):
                        f"{ticks} ticks, scalar C port")
 
 
+def bench_slabs(args, w, sf, dist, rank, world, local, warmup):
+    """N > 1: weak scaling over row slabs.  The scenario is the N = 1 workload stacked N times in y
+    (same width, density, fields), so every rank owns the N = 1 amount of su and pedestrians, and
+    the ranks exchange halos with their ring neighbours every tick (paper_1803_04782_b200/slabs.py,
+    NCCL send/recv on the engines' own device buffers)."""
+    import re
+
+    import torch
+
+    from paper_1803_04782_b200 import slabs
+
+    gw, gh = map(int, re.search(r"grid = (\d+)x(\d+)", w["text"]).groups())
+    text = re.sub(r"grid = \d+x\d+", f"grid = {gw}x{gh * world}", w["text"])
+    cfg = sf.parse_scenario(text)
+    state = sf.seed_population(cfg)
+    P, C = state.population, gw * gh * world
+    runner = slabs.SlabRunner(sf, cfg, state, dist, rank, world, local)
+    for _ in range(warmup):
+        runner.run(TICKS_PER_STEP)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    barrier(dist, local)
+    sampler.recording = True
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        runner.run(TICKS_PER_STEP)  # ends with a stream synchronise
+    torch.cuda.synchronize(local)
+    dt = time.perf_counter() - t0
+    barrier(dist, local)
+    sampler.recording = False
+    clocks = sampler.stop()
+    dt = reduce_max(dist, local, dt)
+    if rank != 0:
+        return 0
+    ticks = TICKS_PER_STEP * args.steps
+    value = P * ticks / dt
+    peak, peak_src = measured_peaks()
+    tick_gbs = (BYTES_PER_SU_TICK * C + BYTES_PER_PED_TICK * P) / (dt / ticks) / 1e9
+    line = {
+        "metric": "pedestrian-steps/s", "value": value, "unit": "pedestrian-steps/s", "su_updates_per_s": value * C / P,
+        "n_gpus": world, "steps": args.steps, "warmup": warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 scores and field sums, f32 field images, i32 occupancy",
+        "data": "synthetic (seeded scenario, seed 42)",
+        "config": {"workload": w["label"] + f" — stacked {world}x in y ({gw}x{gh * world} su, {P} pedestrians)",
+                   "ticks_per_step": TICKS_PER_STEP, "cells": C, "pedestrians": P,
+                   "parallelism": f"{world} row slabs, one per GPU, halo exchange per tick (NCCL send/recv)",
+                   "timing": "host-driven tick loop: wall clock between barriers with device synchronisation, max over ranks",
+                   "l2": "per-GPU working set as at N = 1 (134 MB vs 126 MB L2)"},
+        "clocks": clocks,
+        "e2e": {"value": None, "unit": "pedestrian-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "measured at N = 1 only: the host-facing call scatters one whole-grid SimState"},
+        "gpu_launches": None,
+        "tick_us": 1e6 * dt / ticks,
+        "roofline": {"bound": "hbm", "kernel": "whole tick, all ranks", "achieved": tick_gbs, "peak": peak * world,
+                     "unit": "GB/s", "frac": tick_gbs / (peak * world), "traffic": None, "peak_source": peak_src},
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,10 +281,13 @@ def main():
         return 0
 
     rank, world, local, dist = init_dist(args.gpus)
+    os.environ["SFC_DEVICE"] = str(local)  # seeding / static rasterisation of this rank run on its own GPU
     from paper_1803_04782_b200 import socfield as sf
 
     if sf.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device — the socfield B200 engine has no CPU fallback")
+    if world > 1:
+        return bench_slabs(args, w, sf, dist, rank, world, local, warmup)
     cfg, state = build_state(sf, w)
     ecfg_device = local
     engine = sf.Engine(cfg, 0, ecfg_device)

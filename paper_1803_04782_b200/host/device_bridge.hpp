@@ -33,6 +33,39 @@ struct PedColumns {
 
 sfc_config make_config(const GridGeometry& g, const EngineConfig& cfg);
 
+// Raw-pointer view of a SimState for sfc_upload / sfc_download (cols receives the SoA copy of the
+// pedestrian attributes the view points into).
+sfc_state_view view_of(SimState& s, PedColumns& cols);
+
+// One row slab of a scenario on one device, stepped from outside (multi-process / multi-GPU runs:
+// the caller owns the transport of the halo buffers, see paper_1803_04782_b200/slabs.py).
+class SlabEngine {
+public:
+    SlabEngine(const GridGeometry& g, const EngineConfig& cfg, const std::array<FieldSpec, kDynKinds>& templates,
+               int index, int count, int ped_half_h);
+    ~SlabEngine();
+    SlabEngine(const SlabEngine&) = delete;
+    SlabEngine& operator=(const SlabEngine&) = delete;
+
+    void upload(const SimState& s);
+    void download(SimState& s);           // writes the rows and pedestrians this slab owns
+    void begin(long ticks);
+    void step(int which);                 // 0, 1, 2 — see socfield_cuda.h
+    std::pair<std::uintptr_t, std::size_t> buffer(int kind, int edge, bool recv);
+    std::vector<std::int64_t> finish(long first_tick, long ticks); // synchronises; throws on a device-side error
+    int row0() const noexcept { return row0_; }
+    int rows() const noexcept { return rows_; }
+    int halo() const noexcept { return halo_; }
+    bool has_neighbour(int edge) const noexcept;
+    sfc_engine* handle() const noexcept { return h_; }
+
+private:
+    [[noreturn]] void raise(int status) const;
+    sfc_engine* h_ = nullptr;
+    GridGeometry geom_;
+    int row0_ = 0, rows_ = 0, halo_ = 0;
+};
+
 // Throws the socfield exception matching an SFC_E_* status.
 [[noreturn]] void throw_status(int status, const std::string& message, long tick, int phase);
 

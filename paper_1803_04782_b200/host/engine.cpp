@@ -144,11 +144,19 @@ bool states_identical(const SimState& a, const SimState& b, std::string* diagnos
 
 // ------------------------------------------------------------------ state views ------------
 
+namespace bridge {
+sfc_state_view view_of(SimState& s, PedColumns& cols);
+}
+
 namespace {
 
 // Pointers into a SimState for the C ABI.  The const_cast on an input-only view is confined to
-// this function: sfc_upload never writes through the pointers.
-sfc_state_view make_view(SimState& s, bridge::PedColumns& cols) {
+// the callers: sfc_upload never writes through the pointers.
+sfc_state_view make_view(SimState& s, bridge::PedColumns& cols) { return bridge::view_of(s, cols); }
+
+} // namespace
+
+sfc_state_view bridge::view_of(SimState& s, PedColumns& cols) {
     cols.gather(s.pedestrians);
     sfc_state_view v{};
     v.tick = s.tick;
@@ -166,6 +174,8 @@ sfc_state_view make_view(SimState& s, bridge::PedColumns& cols) {
     v.foot_h = cols.foot_h.data();
     return v;
 }
+
+namespace {
 
 void require_shape(const SimState& s, const GridGeometry& g) {
     const std::size_t cells = static_cast<std::size_t>(g.cells());
@@ -515,3 +525,92 @@ void Engine::verify_state(const SimState& s) const {
 }
 
 } // namespace socfield
+
+// ------------------------------------------------------------------ SlabEngine --------------
+
+namespace socfield::bridge {
+
+SlabEngine::SlabEngine(const GridGeometry& g, const EngineConfig& cfg, const std::array<FieldSpec, kDynKinds>& templates,
+                       int index, int count, int ped_half_h)
+    : geom_(g) {
+    if (count < 2 || index < 0 || index >= count) throw ConfigError("slabs", "need 0 <= index < count and count >= 2");
+    std::array<KindTable, kDynKinds> tables;
+    int field_half_h = 0;
+    for (int k = 0; k < kDynKinds; ++k) {
+        FieldSpec spec = templates[static_cast<std::size_t>(k)];
+        spec.kind = to_field_kind(static_cast<DynKind>(k));
+        tables[static_cast<std::size_t>(k)] = build_kind_table(spec);
+        field_half_h = std::max(field_half_h, spec.geometry.half_h());
+    }
+    halo_ = sfc_slab_halo_rows(field_half_h, ped_half_h, cfg.regulation == Regulation::Linear ? cfg.density_radius : 0);
+    row0_ = static_cast<int>(static_cast<std::int64_t>(g.height) * index / count);
+    rows_ = static_cast<int>(static_cast<std::int64_t>(g.height) * (index + 1) / count) - row0_;
+    sfc_config c = make_config(g, cfg);
+    c.slab_row0 = row0_;
+    c.slab_rows = rows_;
+    c.slab_halo = halo_;
+    sfc_tables t{};
+    for (int k = 0; k < kDynKinds; ++k) t.kind[k] = tables[static_cast<std::size_t>(k)].view();
+    char why[512] = {0};
+    const int status = sfc_create(&c, &t, &h_, why, sizeof why);
+    if (status != SFC_OK) throw_status(status, why, -1, 0);
+}
+
+SlabEngine::~SlabEngine() { sfc_destroy(h_); }
+
+void SlabEngine::raise(int status) const {
+    std::int64_t tick = -1;
+    std::int32_t phase = 0;
+    sfc_error_detail(h_, &tick, &phase, nullptr, nullptr, nullptr);
+    throw_status(status, sfc_last_error(h_), static_cast<long>(tick), phase);
+}
+
+bool SlabEngine::has_neighbour(int edge) const noexcept {
+    if (geom_.boundary == BoundaryMode::Periodic) return true;
+    return edge == 0 ? row0_ > 0 : row0_ + rows_ < geom_.height;
+}
+
+void SlabEngine::upload(const SimState& s) {
+    PedColumns cols;
+    const sfc_state_view v = view_of(const_cast<SimState&>(s), cols);
+    const int status = sfc_upload(h_, &v);
+    if (status != SFC_OK) raise(status);
+}
+
+void SlabEngine::download(SimState& s) {
+    PedColumns cols;
+    sfc_state_view v = view_of(s, cols);
+    v.static_image = nullptr;
+    const int status = sfc_download(h_, &v);
+    if (status != SFC_OK) raise(status);
+    for (std::size_t i = 0; i < s.pedestrians.size(); ++i)
+        s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
+    s.tick = static_cast<long>(v.tick);
+}
+
+void SlabEngine::begin(long ticks) {
+    const int status = sfc_slab_begin(h_, ticks);
+    if (status != SFC_OK) raise(status);
+}
+
+void SlabEngine::step(int which) {
+    const int status = sfc_slab_step(h_, which);
+    if (status != SFC_OK) raise(status);
+}
+
+std::pair<std::uintptr_t, std::size_t> SlabEngine::buffer(int kind, int edge, bool recv) {
+    void* ptr = nullptr;
+    std::size_t bytes = 0;
+    const int status = sfc_slab_buffer(h_, kind, edge, recv ? 1 : 0, &ptr, &bytes);
+    if (status != SFC_OK) raise(status);
+    return {reinterpret_cast<std::uintptr_t>(ptr), bytes};
+}
+
+std::vector<std::int64_t> SlabEngine::finish(long first_tick, long ticks) {
+    std::vector<std::int64_t> moved(static_cast<std::size_t>(std::max(0L, ticks)));
+    const int status = sfc_slab_finish(h_, first_tick, ticks, moved.data());
+    if (status != SFC_OK) raise(status);
+    return moved;
+}
+
+} // namespace socfield::bridge

@@ -312,6 +312,10 @@ sfc_config make_config(const GridGeometry& g, const EngineConfig& cfg) {
     c.rebuild_tolerance = cfg.rebuild_tolerance;
     c.fault_invert_vote_tiebreak = cfg.fault_invert_vote_tiebreak ? 1 : 0;
     c.device = cfg.device;
+    // one process per GPU: free functions that build throw-away engines (seeding, rasterize_static)
+    // carry no device of their own, so a rank can point them at its GPU with SFC_DEVICE
+    if (c.device == 0)
+        if (const char* knob = std::getenv("SFC_DEVICE")) c.device = std::atoi(knob);
     c.slab_row0 = 0;
     c.slab_rows = 0;
     return c;

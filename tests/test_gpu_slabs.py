@@ -44,3 +44,62 @@ def test_slab_halo_too_thin_is_a_config_error(product_lib, monkeypatch):
     with pytest.raises(shim.ShimError) as e:
         gpu.run(1)
     assert e.value.kind == "ConfigError" and "slab_halo" in e.value.message
+
+
+# ---- the multi-process path: one rank per slab, torch.distributed halo exchange ---------------
+
+def _rank_main(rank, world, port, text, ticks, out):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1803_04782_b200 import slabs
+    from paper_1803_04782_b200 import socfield as sf
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # both ranks share GPU 0: halos bounce through the host
+    try:
+        cfg = sf.parse_scenario(text)
+        state = sf.seed_population(cfg)
+        runner = slabs.SlabRunner(sf, cfg, state, dist, rank, world, 0)
+        moved = runner.run(ticks)
+        runner.download(state)  # this rank's rows and pedestrians only
+        eng = runner.engine
+        rows = slice(eng.row0, eng.row0 + eng.rows)
+        out[rank] = dict(moved=list(moved), rows=(eng.row0, eng.rows), occ=state.occupancy()[rows].copy(),
+                         img=[state.image(k)[rows].copy() for k in ("dir-attractive", "dir-repulsive", "recurrent-repulsive")],
+                         centers=state.centers())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("desk64", 2), ("closed-four", 2), ("linear-regulation", 3)])
+def test_multi_process_slabs(name, world):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
+    ticks = 23
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_rank_main, args=(world, port, text, ticks, out), nprocs=world, join=True)
+    cpu = oracle.OracleSim.from_scenario(text)
+    moved = cpu.run(ticks)
+    total = np.sum([np.array(out[r]["moved"]) for r in range(world)], axis=0)
+    np.testing.assert_array_equal(total, moved)
+    owned = np.zeros(cpu.population, bool)
+    for r in range(world):
+        o = out[r]
+        rows = slice(o["rows"][0], o["rows"][0] + o["rows"][1])
+        np.testing.assert_array_equal(o["occ"], cpu.occupancy()[rows])
+        for k in range(3):
+            np.testing.assert_array_equal(bits(o["img"][k]), bits(cpu.image(k)[rows]))
+        truth = cpu.centers()
+        mine = (truth[:, 1] >= o["rows"][0]) & (truth[:, 1] < o["rows"][0] + o["rows"][1])  # pedestrians this rank owns now
+        np.testing.assert_array_equal(o["centers"][mine], truth[mine])
+        owned |= mine
+    assert owned.all()
