@@ -110,7 +110,7 @@ class ClockSampler(threading.Thread):
                 "samples": len(s)}
 
 
-def init_dist(n_gpus: int):
+def init_dist(n_gpus: int, backend: str = "nccl"):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -119,8 +119,13 @@ def init_dist(n_gpus: int):
         import torch
         import torch.distributed as dist_mod
 
-        torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":  # smoke-testing the N > 1 path on a single GPU: all ranks share device 0
+            local = 0
+            torch.cuda.set_device(local)
+            dist_mod.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     return rank, world, local, dist
 
@@ -130,7 +135,8 @@ def reduce_max(dist, local: int, value: float) -> float:
         return value
     import torch
 
-    t = torch.tensor([value], dtype=torch.float64, device=torch.device("cuda", local))
+    on_device = dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=torch.float64, device=torch.device("cuda", local) if on_device else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -139,7 +145,10 @@ def barrier(dist, local: int):
     if dist is not None:
         import torch
 
-        dist.barrier(device_ids=[local])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
         torch.cuda.synchronize(local)
 
 
@@ -208,6 +217,7 @@ def bench_slabs(args, w, sf, dist, rank, world, local, warmup):
     time.sleep(0.2)
     barrier(dist, local)
     sampler.recording = True
+    launches0 = runner.engine.kernel_launches()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         runner.run(TICKS_PER_STEP)  # ends with a stream synchronise
@@ -231,13 +241,13 @@ def bench_slabs(args, w, sf, dist, rank, world, local, warmup):
         "data": "synthetic (seeded scenario, seed 42)",
         "config": {"workload": w["label"] + f" — stacked {world}x in y ({gw}x{gh * world} su, {P} pedestrians)",
                    "ticks_per_step": TICKS_PER_STEP, "cells": C, "pedestrians": P,
-                   "parallelism": f"{world} row slabs, one per GPU, halo exchange per tick (NCCL send/recv)",
+                   "parallelism": f"{world} row slabs, one per GPU, halo exchange per tick ({dist.get_backend()} send/recv)",
                    "timing": "host-driven tick loop: wall clock between barriers with device synchronisation, max over ranks",
                    "l2": "per-GPU working set as at N = 1 (134 MB vs 126 MB L2)"},
         "clocks": clocks,
         "e2e": {"value": None, "unit": "pedestrian-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "measured at N = 1 only: the host-facing call scatters one whole-grid SimState"},
-        "gpu_launches": None,
+        "gpu_launches": runner.engine.kernel_launches() - launches0,  # rank 0's kernels in the timed region
         "tick_us": 1e6 * dt / ticks,
         "roofline": {"bound": "hbm", "kernel": "whole tick, all ranks", "achieved": tick_gbs, "peak": peak * world,
                      "unit": "GB/s", "frac": tick_gbs / (peak * world), "traffic": None, "peak_source": peak_src},
@@ -255,6 +265,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N > 1 slab path with every rank on GPU 0 (single-GPU smoke test of that path)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -280,7 +292,7 @@ def main():
         print(json.dumps(line))
         return 0
 
-    rank, world, local, dist = init_dist(args.gpus)
+    rank, world, local, dist = init_dist(args.gpus, args.dist_backend)
     os.environ["SFC_DEVICE"] = str(local)  # seeding / static rasterisation of this rank run on its own GPU
     from paper_1803_04782_b200 import socfield as sf
 
