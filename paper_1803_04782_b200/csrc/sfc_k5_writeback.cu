@@ -54,8 +54,8 @@ constexpr int kChunkCells = 2048;       // region cells staged per pass (codes 4
 constexpr int kTabSmemMax = 768;        // table entries (all kinds) kept in shared memory
 constexpr int kReplayCap = 1020;        // scatter: work-list capacity for addresses with >= 3 terms
 constexpr int kScatterCells = 256;      // scatter tile = 32 x 8 su
-// shared-memory bytes of the scatter: su x 24 addresses x (double + count byte) + masks + work list
-constexpr int kScatterBytes = kScatterCells * 24 * 8 + kScatterCells * 24 + kScatterCells * 4 + (kReplayCap + 4) * 4;
+// shared-memory bytes of the scatter: su x 24 addresses x double + three term-count bit planes + work list
+constexpr int kScatterBytes = kScatterCells * 24 * 8 + 3 * kScatterCells * 4 + (kReplayCap + 4) * 4;
 
 enum { kModeAll = 0, kModeScatter = 1, kModeDense = 2 };
 
@@ -208,60 +208,83 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
         }
         constexpr int CELLS = kScatterCells;
         double* acc = part;                                                  // [CELLS][24]
-        uint32_t* cnt4 = reinterpret_cast<uint32_t*>(acc + CELLS * 24);      // [CELLS*24/4] 8-bit term counts
-        uint32_t* touched = cnt4 + CELLS * 24 / 4;                           // [CELLS] 24-bit address masks
-        int* replay = reinterpret_cast<int*>(touched + CELLS);               // [kReplayCap]
+        uint32_t* seen1 = reinterpret_cast<uint32_t*>(acc + CELLS * 24);     // [CELLS] addresses with >= 1 term (24-bit masks)
+        uint32_t* seen2 = seen1 + CELLS;                                     // [CELLS] ... >= 2 terms
+        uint32_t* seen3 = seen2 + CELLS;                                     // [CELLS] ... >= 3 terms
+        int* replay = reinterpret_cast<int*>(seen3 + CELLS);                 // [kReplayCap]
         int* n_replay = replay + kReplayCap;
+        uint32_t* const touched = seen1;
         {
             float4* z = reinterpret_cast<float4*>(part);
-            constexpr int N16 = (CELLS * 24 * 8 + CELLS * 24 + CELLS * 4) / 16;
+            constexpr int N16 = (CELLS * 24 * 8 + 3 * CELLS * 4) / 16;
             for (int i = tid; i < N16; i += NT) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (tid == 0) *n_replay = 0;
         }
         __syncthreads();
-        const int IT = a.t.total_entries;
-        for (int r = lane; r < IT; r += 32) {
-            int kind = 0, rb = r;
-            while (kind < kKinds - 1 && rb >= a.t.k[kind].fw * a.t.k[kind].fh) {
-                rb -= a.t.k[kind].fw * a.t.k[kind].fh;
-                ++kind;
+        // lanes take support offsets, warps take events; the table entries of an offset (one per kind)
+        // are fetched once and reused for every event
+        const int BW = 2 * HW + 1, BOX = BW * (2 * HH + 1);
+        for (int o = lane; o < BOX; o += 32) {
+            const int oy = o / BW;
+            const int dx = o - oy * BW - HW, dy = oy - HH; // centre offset = mover - target
+            if ((dx | dy) == 0) continue;
+            uint32_t info[kKinds];
+            double mag[kKinds];
+            int tb = 0;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                const KindTableDev& kt = a.t.k[k];
+                info[k] = 0;
+                mag[k] = 0.0;
+                if (dx >= -kt.hw && dx <= kt.hw && dy >= -kt.hh && dy <= kt.hh) {
+                    const int ti = tb + (dy + kt.hh) * kt.fw + dx + kt.hw;
+                    info[k] = tab_info[ti];
+                    mag[k] = tab_mag[ti];
+                    if (!((info[k] >> 3) & 0xFFu)) info[k] = 0; // outside this kind's support
+                }
+                any = any || info[k] != 0;
+                tb += kt.fw * kt.fh;
             }
-            const uint32_t info = tab_info[r];
-            const uint32_t mask = (info >> 3) & 0xFFu;
-            if (mask == 0) continue; // offset outside the support (incl. the centre)
-            const KindTableDev& kt = a.t.k[kind];
-            const int dy = rb / kt.fw - kt.hh, dx = rb - (dy + kt.hh) * kt.fw - kt.hw;
-            const double mag = tab_mag[r];
-            const int sect = info & 7;
-            const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
+            if (!any) continue;
             for (int e = warp; e < n_events; e += NW) {
                 const uint2 evt = evl[e];
                 const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su = mover - centre offset
                 const int cy = (int)(evt.x >> 16) - dy - HH;
                 if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
-                const uint32_t fb = evt.y & 0xFFu, tb = (evt.y >> 8) & 0xFFu;
-                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-                const bool to = (tb & 0x80u) && ((mask >> ((tb >> shift) & 7u)) & 1u);
-                if (!from && !to) continue;
+                const uint32_t fb = evt.y & 0xFFu, tbyte = (evt.y >> 8) & 0xFFu;
                 const int cell = cy * kTileW + cx;
-                const int addr = cell * 24 + kind * kSects + sect;
-                if (from) atomicAdd(&acc[addr], -mag);
-                if (to) atomicAdd(&acc[addr], mag);
-                atomicAdd(&cnt4[addr >> 2], ((from ? 1u : 0u) + (to ? 1u : 0u)) << (8 * (addr & 3)));
-                atomicOr(&touched[cell], 1u << (kind * kSects + sect));
+#pragma unroll
+                for (int k = 0; k < kKinds; ++k) {
+                    if (info[k] == 0) continue;
+                    const uint32_t mask = (info[k] >> 3) & 0xFFu;
+                    const int shift = k == 0 ? 0 : (k == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
+                    const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                    const bool to = (tbyte & 0x80u) && ((mask >> ((tbyte >> shift) & 7u)) & 1u);
+                    if (!from && !to) continue;
+                    const int a24 = k * kSects + (int)(info[k] & 7u);
+                    const uint32_t bit = 1u << a24;
+                    double* slot = acc + cell * 24 + a24;
+                    if (from) atomicAdd(slot, -mag[k]);
+                    if (to) atomicAdd(slot, mag[k]);
+                    // saturating per-address term count in three bit planes: 1, 2, >= 3
+                    for (int terms = (from ? 1 : 0) + (to ? 1 : 0); terms > 0; --terms) {
+                        if (!(atomicOr(&seen1[cell], bit) & bit)) continue;
+                        if (!(atomicOr(&seen2[cell], bit) & bit)) continue;
+                        atomicOr(&seen3[cell], bit);
+                    }
+                }
             }
         }
         __syncthreads();
         // addresses with three or more terms: exact K-slot replay, one address per thread
-        for (int w = tid; w < CELLS * 24 / 4; w += NT) {
-            const uint32_t v = cnt4[w];
-            if ((v + 0x7D7D7D7Du) & 0x80808080u) { // some byte > 2 (counts stay below 0x80)
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (((v >> (8 * b)) & 0xFFu) > 2u) {
-                        const int slot = atomicAdd(n_replay, 1);
-                        if (slot < kReplayCap) replay[slot] = w * 4 + b;
-                    }
+        for (int cell = tid; cell < CELLS; cell += NT) {
+            uint32_t m = seen3[cell];
+            while (m != 0u) {
+                const int a24 = __ffs((int)m) - 1;
+                m &= m - 1u;
+                const int slot = atomicAdd(n_replay, 1);
+                if (slot < kReplayCap) replay[slot] = cell * 24 + a24;
             }
         }
         __syncthreads();
@@ -270,7 +293,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
         const int rep_items = overflow ? CELLS * 24 : n_rep;
         for (int i = tid; i < rep_items; i += NT) {
             const int addr = overflow ? i : replay[i];
-            if (overflow && ((cnt4[addr >> 2] >> (8 * (addr & 3))) & 0xFFu) <= 2u) continue;
+            if (overflow && !((seen3[addr / 24] >> (addr % 24)) & 1u)) continue;
             const int cell = addr / 24, kind = (addr % 24) / kSects, sect = addr % kSects;
             const int tcx = cell % kTileW + HW, tcy = cell / kTileW + HH;
             const KindTableDev& kt = a.t.k[kind];
