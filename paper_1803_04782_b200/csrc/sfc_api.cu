@@ -52,6 +52,8 @@ struct sfc_engine {
     int* dense_list = nullptr; // k-5 tile ids handed from the scatter to the gather kernel
     int persistent_ctas = 148 * 3;
     int k5_launches = 1;       // kernels per k-5 phase
+    int k5_tile_rows = 8;  // tuning knob, SFC_K5_TILE_ROWS (8 or 4)
+    int k5_scatter_ctas = 148 * 3; // persistent scatter grid; SFC_K5_SCATTER_CTAS (0 = one CTA per tile)
     int k5_event_max = 64; // tuning knob, overridable with SFC_K5_EVENT_MAX (tests force either k-5 path)
     bool uploaded = false;
     long long tick = 0;
@@ -250,6 +252,8 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.ev_max = e->k5_event_max;
     l.dense_list = e->dense_list;
     l.persistent_ctas = e->persistent_ctas;
+    l.tile_rows = e->k5_tile_rows;
+    l.scatter_ctas = e->k5_scatter_ctas;
     return l;
 }
 
@@ -331,6 +335,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = std::atoi(knob);
+    if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
     e->g.H = cfg->height;
@@ -400,6 +405,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         cudaDeviceProp prop{};
         if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->persistent_ctas = prop.multiProcessorCount * 3;
         e->k5_launches = k5_kernels_per_launch(e->tabs, e->k5_event_max);
+        e->k5_scatter_ctas = 1 << 30; // one CTA per tile measured faster than a persistent grid (profiles/README.md)
+        if (const char* knob = std::getenv("SFC_K5_SCATTER_CTAS")) e->k5_scatter_ctas = std::atoi(knob) > 0 ? std::atoi(knob) : (1 << 30);
     }
     if (rc != SFC_OK) return bail(rc);
     cu(cudaMemset(e->ctl, 0, sizeof(Ctl)), "cudaMemset");

@@ -180,6 +180,8 @@ struct K5Launch {
     int ev_max;       // k-5: event-count threshold between the scatter and the gather formulation
     int* dense_list;  // k-5: tile ids for the gather kernel (k5_tile_count entries), or nullptr
     int persistent_ctas; // k-5: grid of the persistent gather kernel
+    int tile_rows;       // k-5: 8 (default) or 4 rows per tile on the two-kernel path
+    int scatter_ctas;    // k-5: grid of the persistent scatter kernel
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);

@@ -42,6 +42,8 @@
 // Regions too large for shared memory (very large fields) use 32 x 4 tiles, gather only, with the
 // region staged in column chunks: the list is sorted, so chunks arrive in order.
 
+#include <cstdlib>
+
 #include "sfc_internal.cuh"
 
 namespace sfc {
@@ -53,9 +55,9 @@ constexpr int kBlockW = 8, kBlockH = 4; // su block owned by one warp at a time 
 constexpr int kChunkCells = 2048;       // region cells staged per pass (codes 4 KB + list 16 KB)
 constexpr int kTabSmemMax = 768;        // table entries (all kinds) kept in shared memory
 constexpr int kReplayCap = 1020;        // scatter: work-list capacity for addresses with >= 3 terms
-constexpr int kScatterCells = 256;      // scatter tile = 32 x 8 su
+constexpr int kOboxMax = 512;           // scatter: decoded support offsets of the largest field box
 // shared-memory bytes of the scatter: su x 24 addresses x double + three term-count bit planes + work list
-constexpr int kScatterBytes = kScatterCells * 24 * 8 + 3 * kScatterCells * 4 + (kReplayCap + 4) * 4;
+constexpr size_t scatter_bytes(int cells) { return (size_t)cells * 24 * 8 + 3 * (size_t)cells * 4 + (kReplayCap + 4) * 4; }
 
 enum { kModeAll = 0, kModeScatter = 1, kModeDense = 2 };
 
@@ -73,6 +75,8 @@ struct K5Args {
     int tab_smem;     // contributor tables fit in shared memory
     int part_doubles; // size of the partial-sum / scatter region, in doubles
     int ev_max;       // scatter handles tiles with at most this many events in reach
+    int debug_stop;   // profiling only (results invalid): leave the scatter kernel after phase N
+    int n_tiles;      // tiles_x * tiles_y
 };
 
 struct Smem {
@@ -193,7 +197,76 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
     };
 
     int n_events = 0;
-    if (single_pass) {
+    if constexpr (MODE == kModeScatter) {
+        // The scatter does not need the events in order (only its rare exact replays do), so the
+        // region is read straight from the event map — rows on warps, columns on lanes — and the
+        // non-zero cells are appended to a list with a shared-memory counter.
+        int* const n_list = colstart;                       // [0]: running count
+        uint2* const unsorted = reinterpret_cast<uint2*>(codes + kOboxMax); // [cap]
+        if (tid == 0) *n_list = 0;
+        __syncthreads();
+        // every load of a thread is issued before the first result is used: one L2 round trip, not one per cell
+        constexpr int LOADS = (kChunkCells + NT - 1) / NT;
+        const bool narrow = RW <= g.W;
+        const int ncell = RW * RH;
+        uint32_t got[LOADS];
+#pragma unroll
+        for (int q = 0; q < LOADS; ++q) {
+            const int i = q * NT + tid;
+            got[q] = 0u;
+            if (i < ncell) {
+                const int ry = i / RW, rc = i - ry * RW;
+                int x = xs + rc;
+                long long idx = -1;
+                if (narrow) {
+                    const long long row = cell_index(g, 0, ys + ry); // -1: row does not exist
+                    if (g.closed) {
+                        if (row >= 0 && x >= 0 && x < g.W) idx = row + x;
+                    } else if (row >= 0) {
+                        x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
+                        idx = row + x;
+                    }
+                } else {
+                    idx = cell_index(g, x, ys + ry);
+                }
+                if (idx >= 0) got[q] = __ldg(ev16 + idx);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < LOADS; ++q) {
+            if (got[q] == 0u) continue;
+            const int i = q * NT + tid;
+            const int ry = i / RW, rc = i - ry * RW;
+            unsorted[atomicAdd(n_list, 1)] = make_uint2((uint32_t)rc | ((uint32_t)ry << 16), got[q]);
+        }
+        __syncthreads();
+        n_events = *n_list;
+        if (a.debug_stop == 7) return;
+        if (n_events == 0) return; // nobody moved within reach of this tile
+        if (n_events > a.ev_max) { // dense tile: hand it to the gather kernel
+            if (tid == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
+            return;
+        }
+        // rank sort by (x, y): every region cell appears once, so keys are unique
+        for (int i = tid; i < n_events; i += NT) {
+            const uint2 mine = unsorted[i];
+            const uint32_t key = ((mine.x & 0xFFFFu) << 16) | (mine.x >> 16);
+            int rank = 0;
+            for (int j = 0; j < n_events; ++j) {
+                const uint32_t xj = unsorted[j].x;
+                rank += ((((xj & 0xFFFFu) << 16) | (xj >> 16)) < key) ? 1 : 0;
+            }
+            evl[rank] = mine;
+        }
+        if (a.debug_stop == 1) return;
+        // support offsets of the largest box, decoded once per CTA: (dx + 128) | (dy + 128) << 8
+        const int BW = 2 * HW + 1, BOX = BW * (2 * HH + 1);
+        for (int o = tid; o < BOX; o += NT) {
+            const int oy = o / BW;
+            codes[o] = (uint16_t)((o - oy * BW - HW + 128) | ((oy - HH + 128) << 8));
+        }
+        __syncthreads();
+    } else if (single_pass) {
         n_events = build_list(0, RW);
         if (n_events == 0) return; // nobody moved within reach of this tile
     }
@@ -202,11 +275,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
     // SCATTER
     // =========================================================================================
     if constexpr (MODE == kModeScatter) {
-        if (n_events > a.ev_max) { // dense tile: hand it to the gather kernel
-            if (tid == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
-            return;
-        }
-        constexpr int CELLS = kScatterCells;
+        constexpr int CELLS = kTileW * MH;
         double* acc = part;                                                  // [CELLS][24]
         uint32_t* seen1 = reinterpret_cast<uint32_t*>(acc + CELLS * 24);     // [CELLS] addresses with >= 1 term (24-bit masks)
         uint32_t* seen2 = seen1 + CELLS;                                     // [CELLS] ... >= 2 terms
@@ -221,62 +290,55 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             if (tid == 0) *n_replay = 0;
         }
         __syncthreads();
-        // lanes take support offsets, warps take events; the table entries of an offset (one per kind)
-        // are fetched once and reused for every event
+        if (a.debug_stop == 2) return;
+        // threads take (event, support offset) pairs — evenly packed whatever the event count
         const int BW = 2 * HW + 1, BOX = BW * (2 * HH + 1);
-        for (int o = lane; o < BOX; o += 32) {
-            const int oy = o / BW;
-            const int dx = o - oy * BW - HW, dy = oy - HH; // centre offset = mover - target
+        const int pairs = n_events * BOX;
+        const float inv_box = 1.0f / (float)BOX;
+        for (int pr = tid; pr < pairs; pr += NT) {
+            int e = (int)(((float)pr + 0.5f) * inv_box);
+            if (e * BOX > pr) --e;
+            else if ((e + 1) * BOX <= pr) ++e;
+            const uint32_t packed = codes[pr - e * BOX];
+            const int dx = (int)(packed & 0xFFu) - 128, dy = (int)(packed >> 8) - 128; // centre offset = mover - target
             if ((dx | dy) == 0) continue;
-            uint32_t info[kKinds];
-            double mag[kKinds];
+            const uint2 evt = evl[e];
+            const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su
+            const int cy = (int)(evt.x >> 16) - dy - HH;
+            if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
+            const uint32_t fb = evt.y & 0xFFu, tbyte = (evt.y >> 8) & 0xFFu;
+            const int cell = cy * kTileW + cx;
             int tb = 0;
-            bool any = false;
 #pragma unroll
             for (int k = 0; k < kKinds; ++k) {
                 const KindTableDev& kt = a.t.k[k];
-                info[k] = 0;
-                mag[k] = 0.0;
-                if (dx >= -kt.hw && dx <= kt.hw && dy >= -kt.hh && dy <= kt.hh) {
-                    const int ti = tb + (dy + kt.hh) * kt.fw + dx + kt.hw;
-                    info[k] = tab_info[ti];
-                    mag[k] = tab_mag[ti];
-                    if (!((info[k] >> 3) & 0xFFu)) info[k] = 0; // outside this kind's support
-                }
-                any = any || info[k] != 0;
+                const int ti = tb + (dy + kt.hh) * kt.fw + dx + kt.hw;
+                const bool inside = dx >= -kt.hw && dx <= kt.hw && dy >= -kt.hh && dy <= kt.hh;
                 tb += kt.fw * kt.fh;
-            }
-            if (!any) continue;
-            for (int e = warp; e < n_events; e += NW) {
-                const uint2 evt = evl[e];
-                const int cx = (int)(evt.x & 0xFFFFu) - dx - HW; // target su = mover - centre offset
-                const int cy = (int)(evt.x >> 16) - dy - HH;
-                if (cx < 0 || cx >= nx || cy < 0 || cy >= ny) continue;
-                const uint32_t fb = evt.y & 0xFFu, tbyte = (evt.y >> 8) & 0xFFu;
-                const int cell = cy * kTileW + cx;
-#pragma unroll
-                for (int k = 0; k < kKinds; ++k) {
-                    if (info[k] == 0) continue;
-                    const uint32_t mask = (info[k] >> 3) & 0xFFu;
-                    const int shift = k == 0 ? 0 : (k == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
-                    const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-                    const bool to = (tbyte & 0x80u) && ((mask >> ((tbyte >> shift) & 7u)) & 1u);
-                    if (!from && !to) continue;
-                    const int a24 = k * kSects + (int)(info[k] & 7u);
-                    const uint32_t bit = 1u << a24;
-                    double* slot = acc + cell * 24 + a24;
-                    if (from) atomicAdd(slot, -mag[k]);
-                    if (to) atomicAdd(slot, mag[k]);
-                    // saturating per-address term count in three bit planes: 1, 2, >= 3
-                    for (int terms = (from ? 1 : 0) + (to ? 1 : 0); terms > 0; --terms) {
-                        if (!(atomicOr(&seen1[cell], bit) & bit)) continue;
-                        if (!(atomicOr(&seen2[cell], bit) & bit)) continue;
-                        atomicOr(&seen3[cell], bit);
-                    }
+                if (!inside) continue;
+                const uint32_t info = tab_info[ti];
+                const uint32_t mask = (info >> 3) & 0xFFu;
+                if (mask == 0) continue;
+                const int shift = k == 0 ? 0 : (k == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
+                const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                const bool to = (tbyte & 0x80u) && ((mask >> ((tbyte >> shift) & 7u)) & 1u);
+                if (!from && !to) continue;
+                const double mag = tab_mag[ti];
+                const int a24 = k * kSects + (int)(info & 7u);
+                const uint32_t bit = 1u << a24;
+                double* slot = acc + cell * 24 + a24;
+                if (from) atomicAdd(slot, -mag);
+                if (to) atomicAdd(slot, mag);
+                // saturating per-address term count in three bit planes: 1, 2, >= 3
+                for (int terms = (from ? 1 : 0) + (to ? 1 : 0); terms > 0; --terms) {
+                    if (!(atomicOr(&seen1[cell], bit) & bit)) continue;
+                    if (!(atomicOr(&seen2[cell], bit) & bit)) continue;
+                    atomicOr(&seen3[cell], bit);
                 }
             }
         }
         __syncthreads();
+        if (a.debug_stop == 3) return;
         // addresses with three or more terms: exact K-slot replay, one address per thread
         for (int cell = tid; cell < CELLS; cell += NT) {
             uint32_t m = seen3[cell];
@@ -335,16 +397,17 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             acc[addr] = total;
         }
         __syncthreads();
+        if (a.debug_stop == 4) return;
         // apply: one 32-byte sector per touched (su, kind); every load of a thread is issued before
         // the first is consumed
-        constexpr int PAIRS = CELLS * kKinds / NT;
+        constexpr int PAIRS = (CELLS * kKinds + NT - 1) / NT;
         float4 v[PAIRS][2];
         uint32_t km[PAIRS];
         float4* rec[PAIRS];
 #pragma unroll
         for (int q = 0; q < PAIRS; ++q) {
             const int pr = q * NT + tid, kind = pr / CELLS, cell = pr % CELLS;
-            km[q] = (touched[cell] >> (kind * kSects)) & 0xFFu;
+            km[q] = pr < CELLS * kKinds ? (touched[cell] >> (kind * kSects)) & 0xFFu : 0u;
             rec[q] = nullptr;
             if (km[q] != 0) {
                 const long long gcell = cell_index(g, x0 + cell % kTileW, y0 + cell / kTileW);
@@ -507,6 +570,8 @@ __global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
     const int tid = threadIdx.x;
     if (MODE != kModeDense && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
     if (a.ctl->error_code != 0) return;
+    if (MODE == kModeScatter && a.debug_stop == 6) return;
+    if (MODE == kModeDense && (int)blockIdx.x >= a.ctl->dense_count) return; // no dense tile for this CTA
     const Smem sm = carve(smem_raw, a);
     if (a.tab_smem) { // contributor tables: one copy per CTA
         int base = 0;
@@ -519,11 +584,17 @@ __global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
             base += n;
         }
     }
-    __syncthreads();
+    if (MODE != kModeScatter) __syncthreads(); // (the scatter synchronises after its event collection, before any table use)
+    if (MODE == kModeScatter && a.debug_stop == 5) return;
     if constexpr (MODE == kModeDense) { // persistent over the tiles the scatter kernel declined
         const int n = a.ctl->dense_count;
         for (int i = blockIdx.x; i < n; i += gridDim.x) {
             process_tile<K, SG, ROWS, NT, MODE>(a, sm, a.dense_list[i]);
+            __syncthreads();
+        }
+    } else if constexpr (MODE == kModeScatter) { // persistent: a CTA strides over the tiles
+        for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+            process_tile<K, SG, ROWS, NT, MODE>(a, sm, tile);
             __syncthreads();
         }
     } else {
@@ -547,13 +618,14 @@ K5Shape k5_shape(const TablesDev& t) {
     if (s.cap < rh_max) s.cap = rh_max; // at least one column per pass
     s.cap = (s.cap + 31) & ~31;
     s.tab_smem = t.total_entries <= kTabSmemMax;
-    const size_t part_bytes = MODE == kModeScatter ? (size_t)kScatterBytes : sizeof(double) * SG * K * NT;
+    const size_t part_bytes = MODE == kModeScatter ? scatter_bytes(kTileW * kBlockH * ROWS) : sizeof(double) * SG * K * NT;
     s.part_doubles = (int)((part_bytes + 7) / 8);
     size_t b = (size_t)s.part_doubles * 8;
     b += sizeof(uint2) * (size_t)s.cap;
     if (s.tab_smem) b += sizeof(double) * t.total_entries + sizeof(uint32_t) * ((t.total_entries + 1) & ~1);
     b += sizeof(int) * (size_t)((s.rw_max + 2 + 1) & ~1);
     b += sizeof(uint16_t) * (size_t)((s.cap + 1) & ~1);
+    if (MODE == kModeScatter) b += sizeof(uint16_t) * kOboxMax + sizeof(uint2) * (size_t)s.cap + 16; // offsets + unsorted list
     s.smem = (b + 127) & ~(size_t)127;
     return s;
 }
@@ -576,9 +648,15 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     a.tab_smem = sh.tab_smem;
     a.part_doubles = sh.part_doubles;
     a.ev_max = l.ev_max;
+    {
+        static const int stop = std::getenv("SFC_K5_DEBUG_STOP") ? std::atoi(std::getenv("SFC_K5_DEBUG_STOP")) : 0;
+        a.debug_stop = stop;
+    }
     const int tiles_y = (l.g.rows + MH - 1) / MH;
     long long blocks = (long long)a.tiles_x * tiles_y;
+    a.n_tiles = (int)blocks;
     if (MODE == kModeDense && blocks > l.persistent_ctas) blocks = l.persistent_ctas;
+    if (MODE == kModeScatter && blocks > l.scatter_ctas) blocks = l.scatter_ctas;
     k5_writeback_kernel<K, SG, ROWS, NT, MODE><<<(unsigned)blocks, NT, sh.smem, stream>>>(a);
     return cudaGetLastError();
 }
@@ -598,13 +676,16 @@ cudaError_t prepare_one(const TablesDev& t) {
 // Small fields (the whole 32 x 8 tile region is staged at once, tables in shared memory): scatter
 // + dense gather.  Otherwise 32 x 4 tiles, gather only, chunked staging.
 bool two_kernel_path(const TablesDev& t) {
-    return (kTileW + 2 * t.max_hw) * (kBlockH * 2 + 2 * t.max_hh) <= kChunkCells && t.total_entries <= kTabSmemMax;
+    return (kTileW + 2 * t.max_hw) * (kBlockH * 2 + 2 * t.max_hh) <= kChunkCells && t.total_entries <= kTabSmemMax &&
+           (2 * t.max_hw + 1) * (2 * t.max_hh + 1) <= kOboxMax && t.max_hw < 128 && t.max_hh < 128;
 }
 
 template <int K, int SG>
 cudaError_t prepare_k(const TablesDev& t) {
     cudaError_t e = prepare_one<K, SG, 2, 256, kModeScatter>(t);
     if (e == cudaSuccess) e = prepare_one<K, SG, 2, 128, kModeDense>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 1, 256, kModeScatter>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 1, 128, kModeDense>(t);
     if (e == cudaSuccess) e = prepare_one<K, SG, 2, 128, kModeAll>(t);
     if (e == cudaSuccess) e = prepare_one<K, SG, 1, 128, kModeAll>(t);
     return e;
@@ -614,6 +695,11 @@ template <int K, int SG>
 cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
     if (!two_kernel_path(l.t)) return launch_one<K, SG, 1, 128, kModeAll>(s, l);
     if (l.ev_max <= 0 || l.dense_list == nullptr) return launch_one<K, SG, 2, 128, kModeAll>(s, l);
+    if (l.tile_rows == 4) { // 32 x 4 tiles: less shared memory per CTA, more CTAs per SM
+        const cudaError_t e = launch_one<K, SG, 1, 256, kModeScatter>(s, l);
+        if (e != cudaSuccess) return e;
+        return launch_one<K, SG, 1, 128, kModeDense>(s, l);
+    }
     const cudaError_t e = launch_one<K, SG, 2, 256, kModeScatter>(s, l);
     if (e != cudaSuccess) return e;
     return launch_one<K, SG, 2, 128, kModeDense>(s, l);
@@ -645,6 +731,6 @@ cudaError_t launch_k5_writeback(cudaStream_t s, const K5Launch& l) {
 
 // Number of kernels one launch_k5_writeback enqueues, and the tile count the dense list must hold.
 int k5_kernels_per_launch(const TablesDev& t, int ev_max) { return two_kernel_path(t) && ev_max > 0 ? 2 : 1; }
-long long k5_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + 7) / 8); }
+long long k5_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + 3) / 4); }
 
 } // namespace sfc

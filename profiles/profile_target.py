@@ -23,3 +23,5 @@ engine.upload(state)
 engine.step_resident(args.warm)      # let the crowd start moving (graph launches)
 m = engine.step_resident(args.ticks, True)  # plain launches, one kernel per phase
 print("moved per tick:", [x.moved for x in m])
+k5 = [x.phase_us[4] for x in m]
+print("k5 us per tick: avg %.1f min %.1f" % (sum(k5) / len(k5), min(k5)))
