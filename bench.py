@@ -56,6 +56,9 @@ WORKLOADS = {
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
+# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch at config 2, from the committed
+# ncu --set full capture (profiles/r1_k5_ncu_full_c2.txt); not re-measured by the bench run
+K5_DRAM_TRAFFIC_C2 = 53.756416e6 + 3.926784e6
 BYTES_PER_SU_TICK = 200.0     # B_su
 BYTES_PER_PED_TICK = 200.0    # B_ped
 
@@ -380,7 +383,8 @@ def main():
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
         "roofline": {"bound": "hbm", "kernel": "k5_writeback_kernel", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                     "traffic": K5_DRAM_TRAFFIC_C2 if args.workload == "c2" else None,
                      "peak_source": peak_src, "bytes_per_launch": BYTES_PER_SU_K5 * C,
                      "whole_tick_gbs": tick_gbs, "whole_tick_frac": tick_gbs / peak},
         "cpu_baseline": cpu,
