@@ -53,6 +53,18 @@ WORKLOADS = {
         label="paper baseline: 500k pedestrians, 1000x1000 su, rho 0.5, eight directions, 7x7",
         text="grid = 1000x1000\ndensity = 0.5\ndirections = eight\nfield_geometry = 7x7\nseed = 42\nrebuild_interval = 50\n",
         cells=1000 * 1000, peds=500000, field=(7, 7)),
+    # BASELINE.json configs[2] "c3": 35x35 fields (support 1224 su) — the paper's one-step cache would need 1432 GiB
+    "c3": dict(
+        label="large plaza: 200k pedestrians, 8192x8192 su, eight directions, 35x35 fields, periodic, rebuild 50",
+        text="grid = 8192x8192\ndensity = 0.00298023223876953125\ndirections = eight\nfield_geometry = 35x35\n"
+             "seed = 42\nrebuild_interval = 50\n",
+        cells=8192 * 8192, peds=200000, field=(35, 35), ticks_per_step=10, ref_ticks_per_step=1),
+    # BASELINE.json configs[4] "c5": 77x77 fields, linear regulation, dense crowd
+    "c5": dict(
+        label="fine-resolution stress: 838 860 pedestrians, 4096x4096 su, rho 0.05, 77x77 fields, linear regulation r=3",
+        text="grid = 4096x4096\ndensity = 0.05\ndirections = eight\nfield_geometry = 77x77\nregulation = linear\n"
+             "density_radius = 3\nseed = 42\nrebuild_interval = 0\n",
+        cells=4096 * 4096, peds=838860, field=(77, 77), ticks_per_step=2, ref_ticks_per_step=1),
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
@@ -272,6 +284,9 @@ def main():
                     help="gloo: run the N > 1 slab path with every rank on GPU 0 (single-GPU smoke test of that path)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
+    global TICKS_PER_STEP, REF_TICKS_PER_STEP
+    TICKS_PER_STEP = w.get("ticks_per_step", TICKS_PER_STEP)
+    REF_TICKS_PER_STEP = w.get("ref_ticks_per_step", REF_TICKS_PER_STEP)
     warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
     if args.impl == "reference":
@@ -334,7 +349,7 @@ def main():
     # ---- per-phase split and the k-5 roofline (CUDA events around every phase) ----------------
     phase = engine.step_resident(TICKS_PER_STEP, True)
     phase_us = [sum(m.phase_us[p] for m in phase) / len(phase) for p in range(5)]
-    plain = [m for m in phase if (m.tick + 1) % 50 != 0]  # ticks whose k-5 slot holds no rebuild
+    plain = [m for m in phase if (m.tick + 1) % 50 != 0] or phase  # ticks whose k-5 slot holds no rebuild
     k5_us = sum(m.phase_us[4] for m in plain) / len(plain)
     peak, peak_src = measured_peaks()
     achieved = BYTES_PER_SU_K5 * C / (k5_us * 1e-6) / 1e9 if k5_us > 0 else None
@@ -360,7 +375,7 @@ def main():
         return 0
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        r = cpu_reference(w, REF_TICKS_PER_STEP, 8, 1)
+        r = cpu_reference(w, REF_TICKS_PER_STEP, 8 if args.workload in ("c1", "c2") else 1, 1 if args.workload in ("c1", "c2") else 0)
         cpu = {"value": r["value"], "unit": "pedestrian-steps/s", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
     line = {
         "metric": "pedestrian-steps/s", "value": value, "unit": "pedestrian-steps/s",

@@ -55,6 +55,9 @@ struct sfc_engine {
     int k5_tile_rows = 8;  // tuning knob, SFC_K5_TILE_ROWS (8 or 4)
     int k5_scatter_ctas = 148 * 3; // persistent scatter grid; SFC_K5_SCATTER_CTAS (0 = one CTA per tile)
     int k5_event_max = 64; // tuning knob, overridable with SFC_K5_EVENT_MAX (tests force either k-5 path)
+    int k5_window = 1;     // 1: window kernel + dense gather; 0 (SFC_K5_PATH=scatter): legacy scatter + gather
+    TileMarks marks{};     // active-tile list of k-5 (epoch stamps + list), written by k-4
+    int sm_count = 148;
     bool uploaded = false;
     long long tick = 0;
     sfc_counters counters{};
@@ -254,6 +257,8 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.persistent_ctas = e->persistent_ctas;
     l.tile_rows = e->k5_tile_rows;
     l.scatter_ctas = e->k5_scatter_ctas;
+    l.marks = e->marks;
+    l.window_path = e->k5_window;
     return l;
 }
 
@@ -261,7 +266,7 @@ int enqueue_tick_kernels(sfc_engine* e) {
     const DebugArrays none{};
     SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
     SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
-    SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
+    SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab, e->marks));
     SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
     return SFC_OK;
 }
@@ -334,8 +339,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     };
     e->cfg = *cfg;
     e->device = cfg->device;
-    if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = std::atoi(knob);
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
+    if (const char* knob = std::getenv("SFC_K5_PATH")) e->k5_window = std::string(knob) != "scatter";
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
     e->g.H = cfg->height;
@@ -386,6 +391,31 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
     cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
     cu(dev_alloc(&e->dense_list, k5_tile_count(e->g)), "cudaMalloc(dense tile list)");
+    e->k5_window = e->k5_window && k5_window_supported(e->tabs);
+    if (e->k5_window) { // active-tile list: 32 x 4 su tiles over the owned rows
+        TileMarks& m = e->marks;
+        m.tiles_x = (e->g.W + kMarkTileW - 1) / kMarkTileW;
+        m.tiles_y = (e->g.rows + kMarkTileH - 1) / kMarkTileH;
+        m.hw = e->tabs.max_hw;
+        m.hh = e->tabs.max_hh;
+        m.edge_lo = 0;
+        m.edge_hi = m.tiles_y;
+        if (e->slab.active) { // tiles whose field region reaches into the halo rows
+            m.edge_lo = std::min(m.tiles_y, (m.hh + kMarkTileH - 1) / kMarkTileH);
+            const int v = e->g.rows - (kMarkTileH - 1) - m.hh;
+            m.edge_hi = std::clamp(v <= 0 ? 0 : (v + kMarkTileH - 1) / kMarkTileH, m.edge_lo, m.tiles_y);
+        }
+        const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
+        cu(dev_alloc(&m.epoch, n_tiles), "cudaMalloc(tile epochs)");
+        cu(dev_alloc(&m.list, n_tiles), "cudaMalloc(active tile list)");
+        if (rc == SFC_OK) cu(cudaMemset(m.epoch, 0, sizeof(int) * (size_t)n_tiles), "cudaMemset");
+        // events per tile region above which nearly every address needs the exact K-slot walk:
+        // about 4.5 events per field window
+        const long long region = (long long)(kMarkTileW + 2 * m.hw) * (kMarkTileH + 2 * m.hh);
+        const long long window = (long long)(2 * m.hw + 1) * (2 * m.hh + 1);
+        e->k5_event_max = (int)std::clamp<long long>(9 * region / (2 * window), 8, 1 << 20);
+    }
+    if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = std::atoi(knob);
     if (e->slab.active) {
         const long long band = (long long)e->g.W * (2 * e->g.halo) + 1;
         e->halo_capacity = (int)std::min<long long>(band, 1 << 18);
@@ -403,8 +433,11 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     }
     {
         cudaDeviceProp prop{};
-        if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->persistent_ctas = prop.multiProcessorCount * 3;
-        e->k5_launches = k5_kernels_per_launch(e->tabs, e->k5_event_max);
+        if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) {
+            e->persistent_ctas = prop.multiProcessorCount * 3;
+            e->sm_count = prop.multiProcessorCount;
+        }
+        e->k5_launches = e->k5_window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max);
         e->k5_scatter_ctas = 1 << 30; // one CTA per tile measured faster than a persistent grid (profiles/README.md)
         if (const char* knob = std::getenv("SFC_K5_SCATTER_CTAS")) e->k5_scatter_ctas = std::atoi(knob) > 0 ? std::atoi(knob) : (1 << 30);
     }
@@ -415,6 +448,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(cudaMemset(e->dyn, 0, sizeof(float) * (size_t)e->cells * kKinds * kSects), "cudaMemset");
     cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
     cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
+    if (e->k5_window) cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
     if (rc == SFC_OK) rc = ensure_peds(e, 0);
     if (rc == SFC_OK) rc = ensure_moved(e, 1);
@@ -436,6 +470,8 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->ev);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
+    cudaFree(e->marks.epoch);
+    cudaFree(e->marks.list);
     for (int edge = 0; edge < 2; ++edge)
         for (int kind = 0; kind < 2; ++kind) {
             cudaFree(e->halo_send[edge][kind]);
@@ -524,6 +560,8 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
                                          "4*(pedestrian half-height+1) + density radius) rows)");
     }
     SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
+    if (e->marks.epoch) // the tick counter may restart: forget every epoch stamp
+        SFC_CUDA(cudaMemsetAsync(e->marks.epoch, 0, sizeof(int) * (size_t)e->marks.tiles_x * e->marks.tiles_y, e->stream));
     Ctl h{};
     h.tick = v->tick;
     h.run_base = v->tick;
@@ -618,7 +656,7 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
             SFC_CUDA(cudaEventRecord(ev[2], e->stream));
             SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
             SFC_CUDA(cudaEventRecord(ev[3], e->stream));
-            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab, e->marks));
             SFC_CUDA(cudaEventRecord(ev[4], e->stream));
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
             if (t == ticks - 1) SFC_CUDA(cudaEventRecord(evs[(size_t)ticks * 5], e->stream));
@@ -691,7 +729,7 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
             e->counters.kernel_launches += 2;
             break;
         case 4:
-            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, e->dbg, e->slab));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, e->dbg, e->slab, e->marks));
             e->counters.kernel_launches += 1;
             break;
         case 5:
@@ -850,7 +888,7 @@ int sfc_slab_step(sfc_engine* e, int step) {
                 if (slab_has_neighbour(e, edge))
                     SFC_CUDA(launch_halo_unpack(e->stream, e->peds, e->ctl, 0, e->halo_recv[edge][0], e->halo_capacity));
             SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
-            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab));
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab, e->marks));
             for (int edge = 0; edge < 2; ++edge)
                 SFC_CUDA(launch_halo_pack(e->stream, e->g, e->peds, e->ctl, edge, 1, depth, e->halo_send[edge][1], e->halo_capacity));
             e->counters.kernel_launches += 8;

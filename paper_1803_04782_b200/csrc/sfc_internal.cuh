@@ -132,6 +132,7 @@ struct Ctl {
     int dense_count;         // k-5: tiles the scatter kernel handed to the gather kernel this tick
     int ev_written_count;    // slab mode: entries of SlabDev::ev_written
     int halo_counts[4];      // slab mode: records packed per (edge, kind): [edge*2 + kind]
+    int active_count;        // k-5: tiles within reach of this tick's movers (TileMarks::list), reset by k-3
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -168,6 +169,25 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, int code, int phase, int x
     }
 }
 
+// k-5 work list.  The su grid is cut into tiles of 32 x 4 su (tile id = tile_y * tiles_x + tile_x,
+// rows counted from the slab's first owned row).  k-4 stamps every tile within field reach of a
+// mover's old or new centre with the tick's epoch and appends it to `list` the first time, so the
+// write-back touches only tiles that can change: its cost follows the movers, not the grid.
+// In slab mode the tiles whose field region reaches into the halo rows ("edge tiles") are not
+// listed — the neighbours' events arrive there as plain row copies — and are always processed.
+constexpr int kMarkTileW = 32, kMarkTileH = 4;
+struct TileMarks {
+    int* epoch;      // [tiles_x * tiles_y] last epoch (tick + 1) the tile was listed in
+    int* list;       // [tiles_x * tiles_y]
+    int tiles_x, tiles_y;
+    int hw, hh;      // field reach (largest half extents over the three kinds)
+    int edge_lo;     // slab mode: tile rows [0, edge_lo) and [edge_hi, tiles_y) are edge tiles
+    int edge_hi;     //            (whole grid: edge_lo = 0, edge_hi = tiles_y)
+};
+__host__ __device__ __forceinline__ int tile_edge_count(const TileMarks& m) {
+    return (m.edge_lo + (m.tiles_y - m.edge_hi)) * m.tiles_x;
+}
+
 // ---- launchers (defined in the .cu files) --------------------------------------------------
 struct K5Launch {
     GridDev g;
@@ -182,13 +202,16 @@ struct K5Launch {
     int persistent_ctas; // k-5: grid of the persistent gather kernel
     int tile_rows;       // k-5: 8 (default) or 4 rows per tile on the two-kernel path
     int scatter_ctas;    // k-5: grid of the persistent scatter kernel
+    TileMarks marks;     // k-5: active-tile list written by k-4 (epoch == nullptr: process every tile)
+    int window_path;     // k-5: 1 = window kernel + dense gather (default), 0 = legacy scatter + gather
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
 cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
                            const DecideParams& dp, const SlabDev& slab);
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
-                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab);
+                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab,
+                           const TileMarks& marks);
 
 // ---- slab halo exchange (sfc_slab.cu) --------------------------------------------------------
 struct HaloRecord {   // 16 bytes: a pedestrian's decision (k-2 -> k-3) or position (k-4 -> next tick)
@@ -229,6 +252,10 @@ cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl);
 cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,
                                  int orientation);
 cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t);
+// window formulation of k-5 (sfc_k5_window.cu)
+bool k5_window_supported(const TablesDev& t);
+cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count);
+cudaError_t launch_k5_window(cudaStream_t s, const K5Launch& a);
 cudaError_t prepare_rebuild(const TablesDev& t);
 
 } // namespace sfc

@@ -693,6 +693,12 @@ cudaError_t prepare_k(const TablesDev& t) {
 
 template <int K, int SG>
 cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
+    if (l.window_path && k5_window_supported(l.t) && l.dense_list != nullptr) {
+        // window kernel over the active tiles; it hands dense tiles (32 x 4) to the gather kernel
+        const cudaError_t e = launch_k5_window(s, l);
+        if (e != cudaSuccess) return e;
+        return launch_one<K, SG, 1, 128, kModeDense>(s, l);
+    }
     if (!two_kernel_path(l.t)) return launch_one<K, SG, 1, 128, kModeAll>(s, l);
     if (l.ev_max <= 0 || l.dense_list == nullptr) return launch_one<K, SG, 2, 128, kModeAll>(s, l);
     if (l.tile_rows == 4) { // 32 x 4 tiles: less shared memory per CTA, more CTAs per SM

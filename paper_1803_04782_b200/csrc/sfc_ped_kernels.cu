@@ -161,6 +161,7 @@ k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const floa
 __global__ void __launch_bounds__(kPedThreads)
 k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault, SlabDev slab) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) ctl->active_count = 0; // k-4 rebuilds the active-tile list of k-5 every tick
     if (i >= p.n) return;
     if (ctl->error_code != 0) return;
     const int d = p.dir[i];
@@ -188,9 +189,53 @@ k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, in
     p.won[i] = won ? 1 : 0;
 }
 
+// Splits the unwrapped interval [lo, hi] of one axis into at most two intervals of wrapped
+// coordinates relative to `origin`, clipped to [0, owned): n = extent of the axis (W or H).
+// Returns the number of intervals written to out[][2].
+__device__ __forceinline__ int wrapped_intervals(int lo, int hi, int n, bool closed, int origin, int owned, int out[2][2]) {
+    int cnt = 0;
+    auto push = [&](int a, int b) { // relative coordinates, clip to the owned range
+        a = max(a, 0);
+        b = min(b, owned - 1);
+        if (a <= b) {
+            out[cnt][0] = a;
+            out[cnt][1] = b;
+            ++cnt;
+        }
+    };
+    if (closed) {
+        push(max(lo, 0) - origin, min(hi, n - 1) - origin);
+    } else if (hi - lo + 1 >= n) {
+        push(0, owned - 1);
+    } else {
+        const int a = emod(lo - origin, n), b = a + (hi - lo);
+        push(a, min(b, n - 1));
+        if (b >= n) push(0, b - n);
+    }
+    return cnt;
+}
+
+// Lists every k-5 tile within field reach of a mover's old or new centre (TileMarks).
+__device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m, Ctl* ctl, int epoch, int fx, int fy, int ux,
+                                           int uy, bool slab_active) {
+    int xr[2][2], yr[2][2];
+    const int nxr = wrapped_intervals(min(fx, fx + ux) - m.hw, max(fx, fx + ux) + m.hw, g.W, g.closed != 0, 0, g.W, xr);
+    const int nyr = wrapped_intervals(min(fy, fy + uy) - m.hh, max(fy, fy + uy) + m.hh, g.H, g.closed != 0, g.row0, g.rows, yr);
+    for (int iy = 0; iy < nyr; ++iy)
+        for (int ty = yr[iy][0] / kMarkTileH; ty <= yr[iy][1] / kMarkTileH; ++ty) {
+            if (slab_active && (ty < m.edge_lo || ty >= m.edge_hi)) continue; // edge tiles are always processed
+            for (int ix = 0; ix < nxr; ++ix)
+                for (int tx = xr[ix][0] / kMarkTileW; tx <= xr[ix][1] / kMarkTileW; ++tx) {
+                    const int t = ty * m.tiles_x + tx;
+                    if (*reinterpret_cast<volatile int*>(m.epoch + t) == epoch) continue;
+                    if (atomicExch(m.epoch + t, epoch) != epoch) m.list[atomicAdd(&ctl->active_count, 1)] = t;
+                }
+        }
+}
+
 __global__ void __launch_bounds__(kPedThreads)
 k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restrict__ ev, Ctl* ctl,
-               unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab) {
+               unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab, TileMarks marks) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool moved = false;
     if (i == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
@@ -233,6 +278,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             if (from >= 0) ev[2 * from] = code;
             if (to >= 0) ev[2 * to + 1] = code;
             p.moved_dir[i] = (int8_t)d;
+            if (marks.epoch) mark_tiles(g, marks, ctl, (int)(ctl->tick % 0x7FFFFFF0ll) + 1, c.x, c.y, ux, uy, slab.active != 0);
             if (slab.active) { // remember the event cells for next tick's clear
                 const int at = atomicAdd(&ctl->ev_written_count, 2);
                 if (at + 1 < slab.ev_capacity) {
@@ -363,8 +409,9 @@ cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p,
 }
 
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
-                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab) {
-    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg, slab);
+                           unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab,
+                           const TileMarks& marks) {
+    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg, slab, marks);
     return cudaGetLastError();
 }
 
