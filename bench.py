@@ -59,6 +59,20 @@ WORKLOADS = {
         text="grid = 8192x8192\ndensity = 0.00298023223876953125\ndirections = eight\nfield_geometry = 35x35\n"
              "seed = 42\nrebuild_interval = 50\n",
         cells=8192 * 8192, peds=200000, field=(35, 35), ticks_per_step=10, ref_ticks_per_step=1),
+    # BASELINE.json configs[3] "c4" at one sixteenth of the area (same density, geometry and fields): the host-seeded
+    # stand-in for the 32768^2 run, which is seeded on the device (--workload c4)
+    "c4r": dict(
+        label="super-large crowd replica: 62 500 pedestrians, 8192x8192 su (c4 density), eight directions, 7x7 fields, rebuild 50",
+        text="grid = 8192x8192\ndensity = 0.000931322574615478515625\ndirections = eight\nfield_geometry = 7x7\n"
+             "seed = 42\nrebuild_interval = 50\n",
+        cells=8192 * 8192, peds=62500, field=(7, 7), ticks_per_step=20, ref_ticks_per_step=1),
+    # BASELINE.json configs[3] "c4": 144 GB of HBM-resident state on ONE B200; the 141 GB host SimState is never built —
+    # the population is seeded straight into HBM (Engine.seed_resident)
+    "c4": dict(
+        label="super-large crowd: 1 000 000 pedestrians, 32768x32768 su, eight directions, 7x7 fields, rebuild 50, seeded on the device",
+        text="grid = 32768x32768\ndensity = 0.000931322574615478515625\ndirections = eight\nfield_geometry = 7x7\n"
+             "seed = 42\nrebuild_interval = 50\n",
+        cells=32768 * 32768, peds=1000000, field=(7, 7), ticks_per_step=10, ref_ticks_per_step=1, resident=True),
     # BASELINE.json configs[4] "c5": 77x77 fields, linear regulation, dense crowd
     "c5": dict(
         label="fine-resolution stress: 838 860 pedestrians, 4096x4096 su, rho 0.05, 77x77 fields, linear regulation r=3",
@@ -318,16 +332,22 @@ def main():
         raise SystemExit("bench.py: no CUDA device — the socfield B200 engine has no CPU fallback")
     if world > 1:
         return bench_slabs(args, w, sf, dist, rank, world, local, warmup)
-    cfg, state = build_state(sf, w)
-    ecfg_device = local
-    engine = sf.Engine(cfg, 0, ecfg_device)
-    P, C = state.population, w["cells"]
+    resident = bool(w.get("resident"))
+    if resident:  # no host SimState at this size
+        cfg, state = sf.parse_scenario(w["text"]), None
+        engine = sf.Engine(cfg, 0, local)
+        P, C = engine.seed_resident(cfg), w["cells"]
+    else:
+        cfg, state = build_state(sf, w)
+        engine = sf.Engine(cfg, 0, local)
+        P, C = state.population, w["cells"]
     assert P == w["peds"], (P, w["peds"])
 
     # ---- device-resident throughput ("value") ------------------------------------------------
     sampler = ClockSampler(local)
     sampler.start()
-    engine.upload(state)
+    if not resident:
+        engine.upload(state)
     for _ in range(warmup):
         engine.step_resident(TICKS_PER_STEP)
     c0 = engine.counters()
@@ -357,15 +377,21 @@ def main():
     tick_gbs = (BYTES_PER_SU_TICK * C + BYTES_PER_PED_TICK * P) / (tick_us * 1e-6) / 1e9
 
     # ---- end to end through Engine.run on host state ("e2e") ---------------------------------
-    engine.download(state)
     e2e_steps = max(3, min(args.steps, 10))
+    if resident:  # the user-facing loop at this size: step the resident state, read the positions back
+        e2e_call = f"socfield.Engine.step_resident({TICKS_PER_STEP}) + download_centers() (the 141 GB SimState is never on the host)"
+        run_e2e = lambda: (engine.step_resident(TICKS_PER_STEP), engine.download_centers())  # noqa: E731
+    else:
+        engine.download(state)
+        e2e_call = f"socfield.Engine.run(state, {TICKS_PER_STEP}) on host SimState (pageable std::vector storage)"
+        run_e2e = lambda: engine.run(state, TICKS_PER_STEP)  # noqa: E731
     for _ in range(2):
-        engine.run(state, TICKS_PER_STEP)
+        run_e2e()
     cb = engine.counters()
     barrier(dist, local)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        engine.run(state, TICKS_PER_STEP)
+        run_e2e()
     barrier(dist, local)
     e2e_s = reduce_max(dist, local, time.perf_counter() - t0)
     ca = engine.counters()
@@ -393,7 +419,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "pedestrian-steps/s",
                 "h2d_bytes_per_step": (ca["h2d_bytes"] - cb["h2d_bytes"]) // e2e_steps,
                 "d2h_bytes_per_step": (ca["d2h_bytes"] - cb["d2h_bytes"]) // e2e_steps,
-                "call": "socfield.Engine.run(state, 100) on host SimState (pageable std::vector storage)"},
+                "call": e2e_call},
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,

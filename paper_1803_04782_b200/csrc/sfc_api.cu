@@ -55,8 +55,13 @@ struct sfc_engine {
     int k5_tile_rows = 8;  // tuning knob, SFC_K5_TILE_ROWS (8 or 4)
     int k5_scatter_ctas = 148 * 3; // persistent scatter grid; SFC_K5_SCATTER_CTAS (0 = one CTA per tile)
     int k5_event_max = 64; // tuning knob, overridable with SFC_K5_EVENT_MAX (tests force either k-5 path)
-    int k5_window = 1;     // 1: window kernel + dense gather; 0 (SFC_K5_PATH=scatter): legacy scatter + gather
-    TileMarks marks{};     // active-tile list of k-5 (epoch stamps + list), written by k-4
+    int k5_window = 0;     // formulation in use: 0 scatter + dense gather kernels, 1 window kernel + dense gather
+    int k5_window_pref = -1; // SFC_K5_PATH: "scatter" 0, "window" 1, unset -1 = by crowd density (sfc_upload)
+    int k5_window_ok = 0;  // the field geometry fits the window kernel
+    int k5_window_event_max = 48; // events per tile region above which the window kernel defers to the dense gather
+    TileMarks marks{};     // active-tile list of k-5 (epoch stamps + list) as the kernels see it; epoch == nullptr: off
+    TileMarks marks_alloc{}; // ... the allocation (the list is only switched on for sparse crowds, see sfc_upload)
+    int k5_active_list = -1; // SFC_K5_ACTIVE_LIST: 0 never, 1 always, -1 by crowd density
     int sm_count = 148;
     bool uploaded = false;
     long long tick = 0;
@@ -252,7 +257,7 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.ctl = e->ctl;
     l.chunk_k = e->cfg.chunk_k;
     l.advance_tick = advance;
-    l.ev_max = e->k5_event_max;
+    l.ev_max = e->k5_window ? e->k5_window_event_max : e->k5_event_max;
     l.dense_list = e->dense_list;
     l.persistent_ctas = e->persistent_ctas;
     l.tile_rows = e->k5_tile_rows;
@@ -340,7 +345,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
-    if (const char* knob = std::getenv("SFC_K5_PATH")) e->k5_window = std::string(knob) != "scatter";
+    if (const char* knob = std::getenv("SFC_K5_PATH")) e->k5_window_pref = std::string(knob) == "window";
+    if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
     e->g.H = cfg->height;
@@ -391,9 +397,9 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
     cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
     cu(dev_alloc(&e->dense_list, k5_tile_count(e->g)), "cudaMalloc(dense tile list)");
-    e->k5_window = e->k5_window && k5_window_supported(e->tabs);
-    if (e->k5_window) { // active-tile list: 32 x 4 su tiles over the owned rows
-        TileMarks& m = e->marks;
+    e->k5_window_ok = e->k5_tile_rows == kMarkTileH && k5_window_supported(e->tabs);
+    if (e->k5_tile_rows == kMarkTileH) { // active-tile list: 32 x 8 su tiles over the owned rows
+        TileMarks& m = e->marks_alloc;
         m.tiles_x = (e->g.W + kMarkTileW - 1) / kMarkTileW;
         m.tiles_y = (e->g.rows + kMarkTileH - 1) / kMarkTileH;
         m.hw = e->tabs.max_hw;
@@ -413,9 +419,9 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         // about 4.5 events per field window
         const long long region = (long long)(kMarkTileW + 2 * m.hw) * (kMarkTileH + 2 * m.hh);
         const long long window = (long long)(2 * m.hw + 1) * (2 * m.hh + 1);
-        e->k5_event_max = (int)std::clamp<long long>(9 * region / (2 * window), 8, 1 << 20);
+        e->k5_window_event_max = (int)std::clamp<long long>(9 * region / (2 * window), 8, 1 << 20);
     }
-    if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = std::atoi(knob);
+    if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = e->k5_window_event_max = std::atoi(knob);
     if (e->slab.active) {
         const long long band = (long long)e->g.W * (2 * e->g.halo) + 1;
         e->halo_capacity = (int)std::min<long long>(band, 1 << 18);
@@ -437,7 +443,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
             e->persistent_ctas = prop.multiProcessorCount * 3;
             e->sm_count = prop.multiProcessorCount;
         }
-        e->k5_launches = e->k5_window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max);
+        e->k5_launches = k5_kernels_per_launch(e->tabs, e->k5_event_max);
         e->k5_scatter_ctas = 1 << 30; // one CTA per tile measured faster than a persistent grid (profiles/README.md)
         if (const char* knob = std::getenv("SFC_K5_SCATTER_CTAS")) e->k5_scatter_ctas = std::atoi(knob) > 0 ? std::atoi(knob) : (1 << 30);
     }
@@ -448,7 +454,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(cudaMemset(e->dyn, 0, sizeof(float) * (size_t)e->cells * kKinds * kSects), "cudaMemset");
     cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
     cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
-    if (e->k5_window) cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
+    if (e->k5_window_ok)
+        cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
     if (rc == SFC_OK) rc = ensure_peds(e, 0);
     if (rc == SFC_OK) rc = ensure_moved(e, 1);
@@ -470,8 +477,8 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->ev);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
-    cudaFree(e->marks.epoch);
-    cudaFree(e->marks.list);
+    cudaFree(e->marks_alloc.epoch);
+    cudaFree(e->marks_alloc.list);
     for (int edge = 0; edge < 2; ++edge)
         for (int kind = 0; kind < 2; ++kind) {
             cudaFree(e->halo_send[edge][kind]);
@@ -524,13 +531,23 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         attr[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
     }
     const long long W = e->g.W;
+    // A view without the dense arrays (occupancy / images NULL) describes a freshly seeded
+    // population: the device derives them itself below (no whole-grid host state needed).
+    if (!v->occupancy) SFC_CUDA(cudaMemsetAsync(e->occ, 0xFF, sizeof(int) * (size_t)C, e->stream));
+    if (!v->static_image) SFC_CUDA(cudaMemsetAsync(e->stat, 0, sizeof(float) * (size_t)C * kSects, e->stream));
     for (const RowSeg& seg : row_segments(e, false)) { // the host arrays cover the whole grid
         const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
-        SFC_CUDA(cudaMemcpyAsync(e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, cudaMemcpyHostToDevice, e->stream));
-        SFC_CUDA(cudaMemcpyAsync(e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects,
-                                 cudaMemcpyHostToDevice, e->stream));
-        e->counters.h2d_bytes += (int64_t)(sizeof(int) * n_seg + sizeof(float) * n_seg * kSects);
+        if (v->occupancy) {
+            SFC_CUDA(cudaMemcpyAsync(e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, cudaMemcpyHostToDevice, e->stream));
+            e->counters.h2d_bytes += (int64_t)(sizeof(int) * n_seg);
+        }
+        if (v->static_image) {
+            SFC_CUDA(cudaMemcpyAsync(e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects,
+                                     cudaMemcpyHostToDevice, e->stream));
+            e->counters.h2d_bytes += (int64_t)(sizeof(float) * n_seg * kSects);
+        }
         for (int k = 0; k < kKinds; ++k) {
+            if (!v->dyn_images[k]) continue;
             for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
                 const long long n = std::min(e->stage_cells, n_seg - c0);
                 SFC_CUDA(cudaMemcpyAsync(e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects,
@@ -560,15 +577,42 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
                                          "4*(pedestrian half-height+1) + density radius) rows)");
     }
     SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
-    if (e->marks.epoch) // the tick counter may restart: forget every epoch stamp
-        SFC_CUDA(cudaMemsetAsync(e->marks.epoch, 0, sizeof(int) * (size_t)e->marks.tiles_x * e->marks.tiles_y, e->stream));
+    if (e->marks_alloc.epoch) {
+        // The list pays when most tiles see no mover in a tick: a mover's field box overlaps about
+        // (w/32 + 1) x (h/8 + 1) tiles, every pedestrian may move.  Dense crowds skip the bookkeeping.
+        const TileMarks& m = e->marks_alloc;
+        const long long per_mover = (long long)((2 * m.hw + 1) / kMarkTileW + 2) * ((2 * m.hh + 1) / kMarkTileH + 2);
+        const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
+        const bool sparse = P * per_mover * 2 < n_tiles;
+        // sparse crowds: the window kernel (its per-tile cost is the lower one when a tile holds an
+        // event or two); otherwise the scatter kernel, which puts a whole CTA on every tile
+        const int window = e->k5_window_ok && (e->k5_window_pref == 1 || (e->k5_window_pref < 0 && sparse));
+        const bool use = window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse);
+        if (use != (e->marks.epoch != nullptr) || window != e->k5_window) {
+            e->marks = use ? m : TileMarks{};
+            e->k5_window = window;
+            e->k5_launches = window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max);
+            e->graph_valid = false;
+        }
+        // the tick counter may restart: forget every epoch stamp
+        SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(int) * (size_t)n_tiles, e->stream));
+    }
     Ctl h{};
     h.tick = v->tick;
     h.run_base = v->tick;
     SFC_CUDA(cudaMemcpyAsync(e->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, e->stream));
+    if (!v->occupancy && P > 0) { // seed_population, scenario.cpp:424
+        SFC_CUDA(launch_occupancy_from_peds(e->stream, e->g, e->peds, e->occ));
+        e->counters.kernel_launches += 1;
+    }
     SFC_CUDA(cudaStreamSynchronize(e->stream)); // gate/attr staging vectors die here
     e->tick = v->tick;
     e->uploaded = true;
+    if (!v->dyn_images[0] || !v->dyn_images[1] || !v->dyn_images[2]) { // rasterize_dynamic, scenario.cpp:427
+        if (v->dyn_images[0] || v->dyn_images[1] || v->dyn_images[2])
+            return fail(e, SFC_E_STATE, "upload: give all three dynamic images or none");
+        return sfc_reset_dynamic_images(e);
+    }
     return SFC_OK;
 }
 

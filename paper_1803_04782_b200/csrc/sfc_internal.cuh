@@ -169,13 +169,13 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, int code, int phase, int x
     }
 }
 
-// k-5 work list.  The su grid is cut into tiles of 32 x 4 su (tile id = tile_y * tiles_x + tile_x,
+// k-5 work list.  The su grid is cut into tiles of 32 x 8 su (tile id = tile_y * tiles_x + tile_x,
 // rows counted from the slab's first owned row).  k-4 stamps every tile within field reach of a
 // mover's old or new centre with the tick's epoch and appends it to `list` the first time, so the
 // write-back touches only tiles that can change: its cost follows the movers, not the grid.
 // In slab mode the tiles whose field region reaches into the halo rows ("edge tiles") are not
 // listed — the neighbours' events arrive there as plain row copies — and are always processed.
-constexpr int kMarkTileW = 32, kMarkTileH = 4;
+constexpr int kMarkTileW = 32, kMarkTileH = 8;
 struct TileMarks {
     int* epoch;      // [tiles_x * tiles_y] last epoch (tick + 1) the tile was listed in
     int* list;       // [tiles_x * tiles_y]
@@ -248,6 +248,7 @@ cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, in
 cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
                                 long long cells);
 cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v);
+cudaError_t launch_occupancy_from_peds(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ);
 cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl);
 cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,
                                  int orientation);

@@ -1,28 +1,29 @@
 // sfc_k5_window.cu — k-5 write-back for sparse-to-moderate crowds (reference engine.cpp:428-472).
 //
 // The reference evaluates, for every (su, kind, sect) address, a list of F contributor offsets
-// against the movement log: 6F probes per su whether anybody moved or not.  Here the unit of work
-// is a WARP on a tile of 32 x 4 su taken from the tick's active-tile list (TileMarks, written by
-// k-4: only tiles within field reach of a mover exist for this kernel).  Everything a warp touches
-// is private to it — no block barriers and no atomics on the data path:
+// against the movement log: 6F probes per su whether anybody moved or not.  Here a CTA of eight
+// warps takes a tile of 32 x 8 su from the tick's active-tile list (TileMarks, written by k-4: only
+// tiles within field reach of a mover exist for this kernel), and every warp owns one block of
+// 8 x 4 su of it — accumulators, counters and image sectors of a block are touched by that warp
+// alone, so the data path has no atomics and only two block barriers per tile:
 //
-//   1. stage    lanes own region columns (tile + field halo).  A lane reads its column of the
-//               2-byte event map straight from global memory (coalesced across lanes), keeps the
-//               codes in shared memory, folds "is there an event" into one 64-bit word per column
-//               and appends its events to the warp's event list.
-//   2. scatter  event by event (warp-uniform loop): the lanes enumerate the su of the tile inside
-//               the event's field box — all distinct, so plain shared-memory read-modify-writes —
-//               and add the gated +-magnitudes of the three kinds to per-(su, kind, sect) doubles,
-//               counting terms per address in 2-bit saturating counters (one 64-bit word per su).
+//   1. stage    (CTA) the tile + field-halo region of the 2-byte event map is read once, coalesced;
+//               the codes go to shared memory, "is there an event" into one 64-bit word per region
+//               column, and every event is appended to the tile's event list.
+//   2. scatter  (warp) event by event (warp-uniform loop, events out of the block's reach skipped):
+//               the lanes enumerate the su of the block inside the event's field box — all
+//               distinct, so plain shared-memory read-modify-writes — and add the gated
+//               +-magnitudes of the three kinds to per-(su, kind, sect) doubles, counting terms
+//               per address in three bit planes (>= 1, >= 2, >= 3 terms).
 //               One or two terms per address are order-independent — whichever StepCache slots
 //               they fall in, the reference's total is fl(t1 + t2) (IEEE addition commutes and
 //               0.0 + t is exact) — so the event order does not matter here.
-//   3. replay   an address with three or more terms is re-walked by the lane that owns the su
-//               through the exact K-slot order (term idx -> slot idx mod K, slots folded in order,
-//               accumulator.hpp:36-46): the lane slides over the column words of its window and
-//               visits the set bits in (dx, dy) lexicographic order, which is the reference's
+//   3. replay   (lane) an address with three or more terms is re-walked by the lane that owns the
+//               su through the exact K-slot order (term idx -> slot idx mod K, slots folded in
+//               order, accumulator.hpp:36-46): the lane slides over the column words of its window
+//               and visits the set bits in (dx, dy) lexicographic order, which is the reference's
 //               contributor-list order (fields.hpp:55-57).
-//   4. apply    image += (float)total on the touched 32-byte sectors only.
+//   4. apply    (lane) image += (float)total on the touched 32-byte sectors only.
 //
 // Tiles whose region holds more events than `ev_max` (dense crowds: nearly every address would be
 // re-walked) are handed to the persistent dense gather kernel of sfc_k5_writeback.cu.
@@ -40,11 +41,12 @@ namespace sfc {
 
 namespace {
 
-constexpr int kWarps = 7;            // warps per CTA (two CTAs per SM); each works on its own tiles
+constexpr int kWarps = 8;            // warps per CTA = 8 x 4 blocks per 32 x 8 tile
+constexpr int kThreads = kWarps * 32;
+constexpr int kBlockW = 8, kBlockH = 4; // su block owned by one warp (one su per lane)
 constexpr int kTabSmemMax = 768;     // table entries (all kinds) kept in shared memory
-constexpr int kHalfW = kMarkTileW / 2;      // the accumulators cover half a tile (16 x 4 su) at a time
-constexpr int kTileSu = kHalfW * kMarkTileH; // 64: su index = row * 16 + x
-constexpr int kEvlMax = 512;         // event-list capacity per warp (ev_max is clamped to it)
+constexpr int kEvlMax = 512;         // event-list capacity per tile (ev_max is clamped to it)
+static_assert(kMarkTileW == 4 * kBlockW && kMarkTileH == 2 * kBlockH, "a tile is 4 x 2 blocks");
 
 struct WinArgs {
     GridDev g;
@@ -57,18 +59,16 @@ struct WinArgs {
     int use_list;
     int ev_max;
     int evl_cap;
-    int same_box;   // the three kinds share one field geometry
     int advance_tick;
     int rwf;        // region columns: 32 + 2 * max_hw
     int rwp;        // row pitch of the staged codes (u16 units)
-    int rh;         // region rows: 4 + 2 * max_hh (<= 64)
-    int warp_bytes; // shared memory per warp
+    int rh;         // region rows: 8 + 2 * max_hh (<= 64)
     int table_bytes;
 };
 
 struct WinShape {
     size_t smem;
-    int rwf, rwp, rh, warp_bytes, table_bytes, tab_smem, evl_cap;
+    int rwf, rwp, rh, table_bytes, tab_smem, evl_cap;
 };
 
 bool same_box(const TablesDev& t) { // the three kinds share one field geometry
@@ -76,6 +76,9 @@ bool same_box(const TablesDev& t) { // the three kinds share one field geometry
 }
 
 int clamp_ev_max(int ev_max) { return ev_max < 0 ? 0 : (ev_max > kEvlMax ? kEvlMax : ev_max); }
+
+constexpr int kAccBytes = kKinds * kSects * 32 * 8; // per warp: [kind * 8 + sect][lane] doubles
+constexpr int kCntBytes = 32 * 16;                  // per warp: term-count bit planes per su
 
 WinShape win_shape(const TablesDev& t, int ev_max) {
     WinShape s;
@@ -86,15 +89,14 @@ WinShape win_shape(const TablesDev& t, int ev_max) {
     s.table_bytes = s.tab_smem ? (int)(sizeof(double) * t.total_entries + sizeof(uint32_t) * 2 * ((t.total_entries + 3) & ~3)) : 0;
     s.table_bytes = (s.table_bytes + 15) & ~15;
     s.evl_cap = (std::max(clamp_ev_max(ev_max), 32) + 3) & ~3;
-    int wb = (int)sizeof(double) * kKinds * kSects * kTileSu;   // acc [kind][sect][su]
-    wb += (int)sizeof(uint4) * kTileSu;                         // term-count bit planes per su
-    wb += (int)sizeof(uint4) * s.evl_cap;                       // event list
-    wb += (int)sizeof(unsigned long long) * s.rwf;              // column words
-    wb += (int)sizeof(long long) * s.rh;                        // su index of each region row
-    wb += 16;                                                   // event counter
-    wb += (int)sizeof(uint16_t) * s.rwp * s.rh;                 // event codes
-    s.warp_bytes = (wb + 15) & ~15;
-    s.smem = (size_t)s.table_bytes + (size_t)kWarps * s.warp_bytes;
+    size_t b = (size_t)s.table_bytes;
+    b += (size_t)kWarps * (kAccBytes + kCntBytes);          // accumulators + counters of the eight blocks
+    b += sizeof(uint4) * (size_t)s.evl_cap;                 // event list
+    b += sizeof(unsigned long long) * (size_t)s.rwf;        // column words
+    b += sizeof(long long) * (size_t)s.rh;                  // su index of each region row
+    b += 16;                                                // event counter
+    b += sizeof(uint16_t) * (size_t)s.rwp * s.rh;           // event codes
+    s.smem = (b + 15) & ~(size_t)15;
     return s;
 }
 
@@ -111,7 +113,7 @@ __device__ __forceinline__ void count_terms(uint4& planes, uint32_t m) {
 // sects and the orientation masks of all kinds, so gating the six possible terms of an (event, su)
 // pair is two ANDs.
 template <int K, bool TAB_SMEM, bool FAST>
-__global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k5_window_kernel(WinArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
         int base = 0;
         for (int k = 0; k < kKinds; ++k) {
             const int n = a.t.k[k].fw * a.t.k[k].fh;
-            for (int i = tid; i < n; i += kWarps * 32) {
+            for (int i = tid; i < n; i += kThreads) {
                 s_mag[base + i] = a.t.k[k].mag[i];
                 s_info[base + i] = a.t.k[k].info[i];
             }
@@ -132,22 +134,22 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
         }
         if (FAST) { // mask(kind 0) | mask(kind 1) << 8 | (kind 2 gated on orientation 0) << 16 | the three sects from bit 17
             const int n = a.t.k[0].fw * a.t.k[0].fh;
-            for (int i = tid; i < n; i += kWarps * 32) {
+            for (int i = tid; i < n; i += kThreads) {
                 const uint32_t i0 = a.t.k[0].info[i], i1 = a.t.k[1].info[i], i2 = a.t.k[2].info[i];
                 const uint32_t m0 = (i0 >> 3) & 0xFFu, m1 = (i1 >> 3) & 0xFFu, m2 = (i2 >> 3) & 1u;
                 s_combo[i] = m0 | (m1 << 8) | (m2 << 16) | ((i0 & 7u) << 17) | ((i1 & 7u) << 20) | ((i2 & 7u) << 23);
             }
         }
-        __syncthreads();
     }
-    unsigned char* const mine = smem_raw + a.table_bytes + (size_t)warp * a.warp_bytes;
-    double* const acc = reinterpret_cast<double*>(mine);                                // [kind * 8 + sect][kTileSu]
-    uint4* const cnt = reinterpret_cast<uint4*>(acc + kKinds * kSects * kTileSu);      // [kTileSu] term-count planes
-    uint4* const evl = cnt + kTileSu;                                                   // [evl_cap]
-    unsigned long long* const colw = reinterpret_cast<unsigned long long*>(evl + a.evl_cap); // [rwf]
-    long long* const rowoff = reinterpret_cast<long long*>(colw + a.rwf);               // [rh] su index of the row's x = 0, -1 none
-    int* const n_list = reinterpret_cast<int*>(rowoff + a.rh);                          // [4]
-    uint16_t* const codes = reinterpret_cast<uint16_t*>(n_list + 4);                    // [rh][rwp]
+    unsigned char* const shared = smem_raw + a.table_bytes;
+    double* const acc = reinterpret_cast<double*>(shared + (size_t)warp * kAccBytes) + lane;   // [kind * 8 + sect] * 32
+    uint4* const cnt_all = reinterpret_cast<uint4*>(shared + (size_t)kWarps * kAccBytes);
+    uint4* const cnt = cnt_all + warp * 32;                                                     // [su of my block]
+    uint4* const evl = cnt_all + kWarps * 32;                                                   // [evl_cap]
+    unsigned long long* const colw = reinterpret_cast<unsigned long long*>(evl + a.evl_cap);   // [rwf]
+    long long* const rowoff = reinterpret_cast<long long*>(colw + a.rwf);                       // [rh] su index of the row's x = 0, -1 none
+    int* const n_list = reinterpret_cast<int*>(rowoff + a.rh);                                  // [4]
+    uint16_t* const codes = reinterpret_cast<uint16_t*>(n_list + 4);                            // [rh][rwp]
 
     const GridDev g = a.g;
     const int HW = a.t.max_hw, HH = a.t.max_hh;
@@ -158,10 +160,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
     const int tiles_x = a.marks.tiles_x;
     const int n_edge = a.use_list ? tile_edge_count(a.marks) : 0;
     const int n_items = a.use_list ? n_edge + a.ctl->active_count : tiles_x * a.marks.tiles_y;
-    const int stride = (int)gridDim.x * kWarps;
     const int tb1 = a.t.k[0].fw * a.t.k[0].fh, tb2 = tb1 + a.t.k[1].fw * a.t.k[1].fh; // table bases of kinds 1, 2
+    const unsigned inv_rwf = 0xFFFFFFFFu / (unsigned)RWF + 1u;
+    // my block of the tile and my su in it
+    const int bx = (warp & 3) * kBlockW, by = (warp >> 2) * kBlockH;
+    const int lx = lane & (kBlockW - 1), ly = lane >> 3;
 
-    for (int item = (int)blockIdx.x * kWarps + warp; item < n_items; item += stride) {
+    for (int item = (int)blockIdx.x; item < n_items; item += (int)gridDim.x) {
         int tile;
         if (!a.use_list) {
             tile = item;
@@ -180,79 +185,33 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
         const int RH = ny + 2 * HH;
         const int xs = x0 - HW, ys = y0 - HH;
 
-        // ---- stage ---------------------------------------------------------------------------
-        for (int ry = lane; ry < RH; ry += 32) rowoff[ry] = cell_index(g, 0, ys + ry); // -1: no such row / not resident
-        for (int c = kMarkTileW + lane; c < RWF; c += 32) colw[c] = 0ull;
-        if (lane == 0) *n_list = 0;
-        __syncwarp();
-        // physical x of a region column, -1 when it does not exist
-        auto column_x = [&](int c) -> int {
-            int x = xs + c;
-            if (g.closed) return (x >= 0 && x < g.W) ? x : -1;
-            if (narrow) return x + (x < 0 ? g.W : (x >= g.W ? -g.W : 0));
-            return emod(x, g.W);
-        };
-        // an event cell: remember its code, list it with the su of the tile inside the largest field box
-        auto found = [&](int c, int ry, uint32_t code) {
-            const int tx0 = max(c - 2 * HW, 0), tx1 = min(c, nx - 1);
-            const int ty0 = max(ry - 2 * HH, 0), ty1 = min(ry, ny - 1);
-            if (tx1 < tx0 || ty1 < ty0) return;
-            const uint32_t fb = code & 0xFFu, tb = code >> 8;
-            const bool hf = fb & 0x80u, ht = tb & 0x80u;
-            // per kind: orientation index of the from / to byte, 8 = no such event (bit 8 of an 8-bit
-            // orientation mask is never set); kind 2 is non-directional: orientation 0 of an all-ones mask
-            const uint32_t f0 = hf ? (fb & 7u) : 8u, f1 = hf ? ((fb >> 3) & 7u) : 8u, f2 = hf ? 0u : 8u;
-            const uint32_t t0 = ht ? (tb & 7u) : 8u, t1 = ht ? ((tb >> 3) & 7u) : 8u, t2 = ht ? 0u : 8u;
-            const int at = atomicAdd(n_list, 1); // the scatter does not care about event order
-            if (at < a.evl_cap)
-                evl[at] = make_uint4((uint32_t)c | ((uint32_t)ry << 9) | ((uint32_t)tx0 << 15) | ((uint32_t)(tx1 - tx0) << 20) |
-                                         ((uint32_t)ty0 << 25) | ((uint32_t)(ty1 - ty0) << 27),
-                                     f0 | (t0 << 4) | (f1 << 8) | (t1 << 12) | (f2 << 16) | (t2 << 20),
-                                     hf ? ((1u << f0) | (256u << f1) | 0x10000u) : 0u,  // selectors into the combined mask word
-                                     ht ? ((1u << t0) | (256u << t1) | 0x10000u) : 0u);
-        };
-        { // the tile's own 32 columns: lane = column, all row loads of a chunk in flight together
-            const int x = column_x(lane);
-            unsigned long long word = 0ull;
-            for (int r0 = 0; r0 < RH; r0 += 16) {
-                uint32_t got[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    got[q] = 0u;
-                    if (r0 + q < RH) {
-                        const long long ro = rowoff[r0 + q];
-                        if (ro >= 0 && x >= 0) got[q] = __ldg(ev16 + ro + x);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    if (r0 + q < RH) {
-                        codes[(r0 + q) * RWP + lane] = (uint16_t)got[q];
-                        if (got[q] != 0u) {
-                            word |= 1ull << (r0 + q);
-                            found(lane, r0 + q, got[q]);
-                        }
-                    }
-                }
-            }
-            colw[lane] = word;
-        }
-        { // the 2 * hw halo columns, flattened over the lanes
-            const int n_extra = (RWF - kMarkTileW) * RH;
-            const unsigned inv_rh = 0xFFFFFFFFu / (unsigned)RH + 1u;
-            for (int i0 = 0; i0 < n_extra; i0 += 128) {
+        // ---- stage (CTA) ---------------------------------------------------------------------
+        __syncthreads(); // the previous tile is done with codes / colw / evl / rowoff (and the tables are loaded)
+        for (int ry = tid; ry < RH; ry += kThreads) rowoff[ry] = cell_index(g, 0, ys + ry); // -1: no such row / not resident
+        for (int c = tid; c < RWF; c += kThreads) colw[c] = 0ull;
+        if (tid == 0) *n_list = 0;
+        __syncthreads();
+        {
+            const int n_cells = RWF * RH;
+            for (int i0 = 0; i0 < n_cells; i0 += 4 * kThreads) {
                 uint32_t got[4];
                 int cq[4], rq[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = i0 + 32 * q + lane;
+                for (int q = 0; q < 4; ++q) { // the loads of the chunk fly together
+                    const int i = i0 + q * kThreads + tid;
                     got[q] = 0u;
                     cq[q] = -1;
-                    if (i < n_extra) {
-                        const int cx = (int)__umulhi((unsigned)i, inv_rh); // i / RH
-                        cq[q] = kMarkTileW + cx;
-                        rq[q] = i - cx * RH;
-                        const int x = column_x(cq[q]);
+                    if (i < n_cells) {
+                        rq[q] = (int)__umulhi((unsigned)i, inv_rwf); // i / RWF
+                        cq[q] = i - rq[q] * RWF;
+                        int x = xs + cq[q];
+                        if (g.closed) {
+                            if (x < 0 || x >= g.W) x = -1;
+                        } else if (narrow) {
+                            x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
+                        } else {
+                            x = emod(x, g.W);
+                        }
                         const long long ro = rowoff[rq[q]];
                         if (ro >= 0 && x >= 0) got[q] = __ldg(ev16 + ro + x);
                     }
@@ -260,53 +219,66 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (cq[q] < 0) continue;
-                    codes[rq[q] * RWP + cq[q]] = (uint16_t)got[q];
-                    if (got[q] != 0u) {
-                        atomicOr(&colw[cq[q]], 1ull << rq[q]);
-                        found(cq[q], rq[q], got[q]);
-                    }
+                    const int c = cq[q], ry = rq[q];
+                    const uint32_t code = got[q];
+                    codes[ry * RWP + c] = (uint16_t)code;
+                    if (code == 0u) continue;
+                    atomicOr(&colw[c], 1ull << ry);
+                    // su of the tile inside the largest field box around the event
+                    const int tx0 = max(c - 2 * HW, 0), tx1 = min(c, nx - 1);
+                    const int ty0 = max(ry - 2 * HH, 0), ty1 = min(ry, ny - 1);
+                    if (tx1 < tx0 || ty1 < ty0) continue;
+                    const uint32_t fb = code & 0xFFu, tb = code >> 8;
+                    const bool hf = fb & 0x80u, ht = tb & 0x80u;
+                    // per kind: orientation index of the from / to byte, 8 = no such event (bit 8 of an
+                    // 8-bit orientation mask is never set); kind 2 is non-directional: orientation 0
+                    const uint32_t f0 = hf ? (fb & 7u) : 8u, f1 = hf ? ((fb >> 3) & 7u) : 8u, f2 = hf ? 0u : 8u;
+                    const uint32_t t0 = ht ? (tb & 7u) : 8u, t1 = ht ? ((tb >> 3) & 7u) : 8u, t2 = ht ? 0u : 8u;
+                    const int at = atomicAdd(n_list, 1); // the scatter does not care about event order
+                    if (at < a.evl_cap)
+                        evl[at] = make_uint4((uint32_t)c | ((uint32_t)ry << 9) | ((uint32_t)tx0 << 15) | ((uint32_t)tx1 << 20) |
+                                                 ((uint32_t)ty0 << 25) | ((uint32_t)ty1 << 28),
+                                             f0 | (t0 << 4) | (f1 << 8) | (t1 << 12) | (f2 << 16) | (t2 << 20),
+                                             hf ? ((1u << f0) | (256u << f1) | 0x10000u) : 0u, // selectors into the combined mask word
+                                             ht ? ((1u << t0) | (256u << t1) | 0x10000u) : 0u);
                 }
             }
         }
-        __syncwarp();
+        __syncthreads();
         const int n_events = *n_list;
         if (n_events == 0) continue;       // (conservative marking: nobody within reach after all)
         if (n_events > a.ev_max) {         // dense tile: exact gather kernel
-            if (lane == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
-            __syncwarp();
+            if (tid == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
             continue;
         }
+        if (bx >= nx || by >= ny) continue; // my block lies outside the grid (partial tile)
+        const int bnx = min(kBlockW, nx - bx), bny = min(kBlockH, ny - by);
 
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-            const int hx0 = half * kHalfW;           // first tile column of this half
-            const int hnx = min(kHalfW, nx - hx0);   // columns of the half inside the grid
-            if (hnx <= 0) break;
-            // ---- scatter ---------------------------------------------------------------------
-            {
-                constexpr int kZero16 = (kKinds * kSects * 8 + 16) * kTileSu / 16; // acc + cnt, contiguous
-                for (int i = lane; i < kZero16; i += 32) reinterpret_cast<uint4*>(acc)[i] = make_uint4(0u, 0u, 0u, 0u);
-            }
-            __syncwarp();
-            for (int e = 0; e < n_events; ++e) {
-                const uint4 evt = evl[e]; // broadcast
-                const int ec = (int)(evt.x & 511u), er = (int)((evt.x >> 9) & 63u);
-                const int tx0 = max((int)((evt.x >> 15) & 31u), hx0);
-                const int tx1 = min((int)((evt.x >> 15) & 31u) + (int)((evt.x >> 20) & 31u), hx0 + hnx - 1);
-                const int w = tx1 - tx0 + 1;
-                if (w <= 0) continue; // uniform: the event does not reach this half
-                const int ty0 = (int)((evt.x >> 25) & 3u), h = (int)((evt.x >> 27) & 3u) + 1;
-                const int n_su = w * h;
-                for (int i = lane; i < n_su; i += 32) {
-                    const int iy = (i >= w) + (i >= 2 * w) + (i >= 3 * w); // h <= 4 rows
-                    const int tx = tx0 + i - iy * w, ty = ty0 + iy;
-                    const int dx = ec - HW - tx, dy = er - HH - ty; // centre offset = mover - target
-                    const int su = ty * kHalfW + tx - hx0;
-                    if (FAST) {
-                        const int tl = (dy + HH) * (2 * HW + 1) + dx + HW;
-                        const uint32_t combo = s_combo[tl];
-                        const uint32_t fbits = combo & evt.z, tbits = combo & evt.w; // gated terms, all kinds
-                        if ((fbits | tbits) == 0u) continue; // (also the centre offset and offsets outside the support)
+        // ---- scatter (warp: my block) --------------------------------------------------------
+#pragma unroll
+        for (int i = 0; i < kKinds * kSects; ++i) acc[i * 32] = 0.0;
+        cnt[lane] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        for (int e = 0; e < n_events; ++e) {
+            const uint4 evt = evl[e]; // broadcast
+            // su of my block inside the event's (largest) field box
+            const int tx0 = max((int)((evt.x >> 15) & 31u), bx), tx1 = min((int)((evt.x >> 20) & 31u), bx + bnx - 1);
+            const int ty0 = max((int)((evt.x >> 25) & 7u), by), ty1 = min((int)((evt.x >> 28) & 7u), by + bny - 1);
+            const int w = tx1 - tx0 + 1, h = ty1 - ty0 + 1;
+            if (w <= 0 || h <= 0) continue; // uniform: the event does not reach my block
+            const int ec = (int)(evt.x & 511u), er = (int)((evt.x >> 9) & 63u);
+            // at most 8 x 4 su: one pass, lane i -> (i % w, i / w)
+            const int iy = (lane >= w) + (lane >= 2 * w) + (lane >= 3 * w);
+            if (lane < w * h) {
+                const int tx = tx0 + lane - iy * w, ty = ty0 + iy;
+                const int dx = ec - HW - tx, dy = er - HH - ty; // centre offset = mover - target
+                const int su = (ty - by) * kBlockW + tx - bx;
+                double* const my = acc - lane + su; // accumulators of that su
+                if (FAST) {
+                    const int tl = (dy + HH) * (2 * HW + 1) + dx + HW;
+                    const uint32_t combo = s_combo[tl];
+                    const uint32_t fbits = combo & evt.z, tbits = combo & evt.w; // gated terms, all kinds
+                    if ((fbits | tbits) != 0u) { // (else: the centre offset, offsets outside the support, other orientations)
                         uint32_t mf = 0u, mt = 0u;
 #pragma unroll
                         for (int k = 0; k < kKinds; ++k) {
@@ -318,147 +290,127 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k5_window_kernel(WinArgs a) {
                             // one or two terms in all: the plain sum IS the reference's total; more: replayed below
                             if (from != to) {
                                 const double mag = s_mag[(k == 0 ? 0 : (k == 1 ? tb1 : tb2)) + tl];
-                                double* const slot = acc + a24 * kTileSu + su;
-                                *slot = __dadd_rn(*slot, from ? -mag : mag); // (-mag + mag would add +0.0)
+                                my[a24 * 32] = __dadd_rn(my[a24 * 32], from ? -mag : mag); // (-mag + mag would add +0.0)
                             }
                         }
                         uint4 planes = cnt[su];
                         count_terms(planes, mf);
                         count_terms(planes, mt);
                         cnt[su] = planes;
-                    } else {
-                        uint4 planes = cnt[su];
-                        int tbase = 0;
-#pragma unroll
-                        for (int k = 0; k < kKinds; ++k) {
-                            const KindTableDev& kt = a.t.k[k];
-                            const int tb = tbase;
-                            tbase += kt.fw * kt.fh;
-                            if (dx < -kt.hw || dx > kt.hw || dy < -kt.hh || dy > kt.hh) continue;
-                            const int tl = (dy + kt.hh) * kt.fw + dx + kt.hw;
-                            const uint32_t info = TAB_SMEM ? s_info[tb + tl] : __ldg(kt.info + tl);
-                            const uint32_t mask = (info >> 3) & 0xFFu;
-                            const bool from = (mask >> ((evt.y >> (8 * k)) & 15u)) & 1u, to = (mask >> ((evt.y >> (8 * k + 4)) & 15u)) & 1u;
-                            if (!from && !to) continue; // (also the centre offset and offsets outside the support: mask 0)
-                            const int a24 = k * kSects + (int)(info & 7u);
-                            if (from != to) {
-                                const double mag = TAB_SMEM ? s_mag[tb + tl] : __ldg(kt.mag + tl);
-                                double* const slot = acc + a24 * kTileSu + su;
-                                *slot = __dadd_rn(*slot, from ? -mag : mag);
-                            }
-                            if (from) count_terms(planes, 1u << a24);
-                            if (to) count_terms(planes, 1u << a24);
-                        }
-                        cnt[su] = planes;
                     }
-                }
-                __syncwarp(); // the next event may touch the same su from another lane
-            }
-
-            // lanes <-> su of the half: two rows of 16 per step
-            const int lx = lane & (kHalfW - 1), lrow = lane >> 4;
-            // ---- replay: addresses with three or more terms, exact K-slot order ------------------
-#pragma unroll 1
-            for (int r2 = 0; r2 < ny; r2 += 2) {
-                const int r = r2 + lrow;
-                const int su = r * kHalfW + lx;
-                uint32_t m3 = (r < ny && lx < hnx) ? cnt[su].z : 0u;
-                while (m3 != 0u) {
-                    const int a24 = __ffs((int)m3) - 1;
-                    m3 &= m3 - 1u;
-                    const int kind = a24 >> 3, sect = a24 & 7;
-                    const KindTableDev& kt = a.t.k[kind];
-                    const int tb = kind == 0 ? 0 : (kind == 1 ? tb1 : tb2);
-                    const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
-                    double p[K];
-                    unsigned used = 0u;
-                    int cc = HW - kt.hw - 1;
-                    const int cc_last = HW + kt.hw;
-                    const int colbase = hx0 + lx; // region column of my window's first column
-                    unsigned long long bits = 0ull;
-                    for (;;) { // my window's events, column by column, rows ascending
-                        while (bits == 0ull && cc < cc_last) {
-                            ++cc;
-                            bits = (colw[colbase + cc] >> r) & hmask;
-                        }
-                        if (bits == 0ull) break;
-                        const int dyp = __ffsll((long long)bits) - 1;
-                        bits &= bits - 1ull;
-                        const int dx = cc - HW, dy = dyp - HH;
-                        if (dy < -kt.hh || dy > kt.hh) continue;
+                } else {
+                    uint4 planes = cnt[su];
+                    int tbase = 0;
+#pragma unroll
+                    for (int k = 0; k < kKinds; ++k) {
+                        const KindTableDev& kt = a.t.k[k];
+                        const int tb = tbase;
+                        tbase += kt.fw * kt.fh;
+                        if (dx < -kt.hw || dx > kt.hw || dy < -kt.hh || dy > kt.hh) continue;
                         const int tl = (dy + kt.hh) * kt.fw + dx + kt.hw;
                         const uint32_t info = TAB_SMEM ? s_info[tb + tl] : __ldg(kt.info + tl);
                         const uint32_t mask = (info >> 3) & 0xFFu;
-                        if (mask == 0u || (int)(info & 7u) != sect) continue;
-                        const uint32_t code = codes[(r + dyp) * RWP + colbase + cc];
-                        const uint32_t fb = code & 0xFFu, tbyte = code >> 8;
-                        const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
-                        const bool to = (tbyte & 0x80u) && ((mask >> ((tbyte >> shift) & 7u)) & 1u);
-                        if (!from && !to) continue;
-                        const double mag = TAB_SMEM ? s_mag[tb + tl] : __ldg(kt.mag + tl);
-                        const uint32_t j2 = (info >> 11) << 1;
-#pragma unroll
-                        for (int hf = 0; hf < 2; ++hf) { // from-term (idx 2j) then to-term (idx 2j+1)
-                            if (!(hf == 0 ? from : to)) continue;
-                            const int slot = (int)((j2 + hf) & (K - 1));
-                            const double term = hf == 0 ? -mag : mag;
-#pragma unroll
-                            for (int q = 0; q < K; ++q) {
-                                if (q != slot) continue;
-                                p[q] = ((used >> q) & 1u) ? __dadd_rn(p[q], term) : term;
-                            }
-                            used |= 1u << slot;
+                        const bool from = (mask >> ((evt.y >> (8 * k)) & 15u)) & 1u, to = (mask >> ((evt.y >> (8 * k + 4)) & 15u)) & 1u;
+                        if (!from && !to) continue; // (also the centre offset and offsets outside the support: mask 0)
+                        const int a24 = k * kSects + (int)(info & 7u);
+                        if (from != to) {
+                            const double mag = TAB_SMEM ? s_mag[tb + tl] : __ldg(kt.mag + tl);
+                            my[a24 * 32] = __dadd_rn(my[a24 * 32], from ? -mag : mag);
                         }
+                        if (from) count_terms(planes, 1u << a24);
+                        if (to) count_terms(planes, 1u << a24);
                     }
-                    double total = 0.0; // StepCache::total, slot order
-#pragma unroll
-                    for (int q = 0; q < K; ++q)
-                        if ((used >> q) & 1u) total = __dadd_rn(total, p[q]);
-                    acc[a24 * kTileSu + su] = total;
+                    cnt[su] = planes;
                 }
             }
-
-            // ---- apply: image += (float)total, one 32-byte sector per touched (su, kind) --------
-            // every touched sector of the half is requested first: one L2 round trip
-            {
-                float4 v[2][kKinds][2];
-                uint32_t crow[2];
-#pragma unroll
-                for (int it = 0; it < 2; ++it) {
-                    const int r = 2 * it + lrow;
-                    crow[it] = (r < ny && lx < hnx) ? cnt[r * kHalfW + lx].x : 0u;
-                    if (crow[it] == 0u) continue;
-                    const float4* rec = reinterpret_cast<const float4*>(a.dyn + (rowoff[r + HH] + x0 + hx0 + lx) * (kKinds * kSects));
-#pragma unroll
-                    for (int k = 0; k < kKinds; ++k) {
-                        if (((crow[it] >> (8 * k)) & 0xFFu) == 0u) continue;
-                        v[it][k][0] = rec[2 * k];
-                        v[it][k][1] = rec[2 * k + 1];
-                    }
-                }
-#pragma unroll
-                for (int it = 0; it < 2; ++it) {
-                    if (crow[it] == 0u) continue;
-                    const int r = 2 * it + lrow;
-                    const int su = r * kHalfW + lx;
-                    float4* rec = reinterpret_cast<float4*>(a.dyn + (rowoff[r + HH] + x0 + hx0 + lx) * (kKinds * kSects));
-#pragma unroll
-                    for (int k = 0; k < kKinds; ++k) {
-                        if (((crow[it] >> (8 * k)) & 0xFFu) == 0u) continue;
-                        float f[8] = {v[it][k][0].x, v[it][k][0].y, v[it][k][0].z, v[it][k][0].w,
-                                      v[it][k][1].x, v[it][k][1].y, v[it][k][1].z, v[it][k][1].w};
-                        // untouched sects hold +0.0: adding it is what the reference does for every address
-#pragma unroll
-                        for (int sct = 0; sct < kSects; ++sct)
-                            f[sct] = __fadd_rn(f[sct], __double2float_rn(acc[(k * kSects + sct) * kTileSu + su]));
-                        rec[2 * k] = make_float4(f[0], f[1], f[2], f[3]);
-                        rec[2 * k + 1] = make_float4(f[4], f[5], f[6], f[7]);
-                    }
-                }
-            }
-            __syncwarp(); // the other half reuses acc / cnt
+            __syncwarp(); // the next event may touch the same su from another lane
         }
-        __syncwarp(); // the next tile's staging overwrites codes / colw / evl
+
+        // ---- replay + apply (lane: my su) ------------------------------------------------------
+        const bool mine = lx < bnx && ly < bny;
+        const uint4 planes = mine ? cnt[lane] : make_uint4(0u, 0u, 0u, 0u);
+        if (__ballot_sync(0xFFFFFFFFu, planes.x != 0u) == 0u) continue; // nothing reached my block
+        float4 v[kKinds][2];
+        float4* rec = nullptr;
+        if (planes.x != 0u) { // request the touched sectors now: they fly while the replay runs
+            rec = reinterpret_cast<float4*>(a.dyn + (rowoff[by + ly + HH] + x0 + bx + lx) * (kKinds * kSects));
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                if (((planes.x >> (8 * k)) & 0xFFu) == 0u) continue;
+                v[k][0] = rec[2 * k];
+                v[k][1] = rec[2 * k + 1];
+            }
+        }
+        {
+            const int r = by + ly;           // my tile row
+            const int colbase = bx + lx;     // region column of my window's first column
+            uint32_t m3 = planes.z;          // addresses with three or more terms: exact K-slot order
+            while (m3 != 0u) {
+                const int a24 = __ffs((int)m3) - 1;
+                m3 &= m3 - 1u;
+                const int kind = a24 >> 3, sect = a24 & 7;
+                const KindTableDev& kt = a.t.k[kind];
+                const int tb = kind == 0 ? 0 : (kind == 1 ? tb1 : tb2);
+                const int shift = kind == 0 ? 0 : (kind == 1 ? 3 : 8); // kind 2: orientation 0 of an all-ones mask
+                double p[K];
+                unsigned used = 0u;
+                int cc = HW - kt.hw - 1;
+                const int cc_last = HW + kt.hw;
+                unsigned long long bits = 0ull;
+                for (;;) { // my window's events, column by column, rows ascending
+                    while (bits == 0ull && cc < cc_last) {
+                        ++cc;
+                        bits = (colw[colbase + cc] >> r) & hmask;
+                    }
+                    if (bits == 0ull) break;
+                    const int dyp = __ffsll((long long)bits) - 1;
+                    bits &= bits - 1ull;
+                    const int dx = cc - HW, dy = dyp - HH;
+                    if (dy < -kt.hh || dy > kt.hh) continue;
+                    const int tl = (dy + kt.hh) * kt.fw + dx + kt.hw;
+                    const uint32_t info = TAB_SMEM ? s_info[tb + tl] : __ldg(kt.info + tl);
+                    const uint32_t mask = (info >> 3) & 0xFFu;
+                    if (mask == 0u || (int)(info & 7u) != sect) continue;
+                    const uint32_t code = codes[(r + dyp) * RWP + colbase + cc];
+                    const uint32_t fb = code & 0xFFu, tbyte = code >> 8;
+                    const bool from = (fb & 0x80u) && ((mask >> ((fb >> shift) & 7u)) & 1u);
+                    const bool to = (tbyte & 0x80u) && ((mask >> ((tbyte >> shift) & 7u)) & 1u);
+                    if (!from && !to) continue;
+                    const double mag = TAB_SMEM ? s_mag[tb + tl] : __ldg(kt.mag + tl);
+                    const uint32_t j2 = (info >> 11) << 1;
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) { // from-term (idx 2j) then to-term (idx 2j+1)
+                        if (!(hf == 0 ? from : to)) continue;
+                        const int slot = (int)((j2 + hf) & (K - 1));
+                        const double term = hf == 0 ? -mag : mag;
+#pragma unroll
+                        for (int q = 0; q < K; ++q) {
+                            if (q != slot) continue;
+                            p[q] = ((used >> q) & 1u) ? __dadd_rn(p[q], term) : term;
+                        }
+                        used |= 1u << slot;
+                    }
+                }
+                double total = 0.0; // StepCache::total, slot order
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+                    if ((used >> q) & 1u) total = __dadd_rn(total, p[q]);
+                acc[a24 * 32] = total;
+            }
+        }
+        if (planes.x != 0u) { // image += (float)total, one 32-byte sector per touched (su, kind)
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                if (((planes.x >> (8 * k)) & 0xFFu) == 0u) continue;
+                float f[8] = {v[k][0].x, v[k][0].y, v[k][0].z, v[k][0].w, v[k][1].x, v[k][1].y, v[k][1].z, v[k][1].w};
+                // untouched sects hold +0.0: adding it is what the reference does for every address
+#pragma unroll
+                for (int sct = 0; sct < kSects; ++sct)
+                    f[sct] = __fadd_rn(f[sct], __double2float_rn(acc[(k * kSects + sct) * 32]));
+                rec[2 * k] = make_float4(f[0], f[1], f[2], f[3]);
+                rec[2 * k + 1] = make_float4(f[4], f[5], f[6], f[7]);
+            }
+        }
     }
 }
 
@@ -478,7 +430,7 @@ cudaError_t prepare_one(const WinShape& sh, int sm_count, WinPrepared& st) {
     }
     int per_sm = 0;
     const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_window_kernel<K, TAB_SMEM, FAST>, kWarps * 32, sh.smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_window_kernel<K, TAB_SMEM, FAST>, kThreads, sh.smem);
     if (e != cudaSuccess) return e;
     st.ctas = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
@@ -505,24 +457,22 @@ cudaError_t launch_k(cudaStream_t stream, const K5Launch& l, const WinPrepared& 
     a.use_list = l.marks.epoch != nullptr;
     a.ev_max = clamp_ev_max(l.ev_max);
     a.evl_cap = sh.evl_cap;
-    a.same_box = same_box(l.t);
     a.advance_tick = l.advance_tick;
     a.rwf = sh.rwf;
     a.rwp = sh.rwp;
     a.rh = sh.rh;
-    a.warp_bytes = sh.warp_bytes;
     a.table_bytes = sh.table_bytes;
     static const int knob = std::getenv("SFC_K5_WINDOW_CTAS") ? std::atoi(std::getenv("SFC_K5_WINDOW_CTAS")) : 0;
-    long long blocks = ((long long)l.marks.tiles_x * l.marks.tiles_y + kWarps - 1) / kWarps;
+    long long blocks = (long long)l.marks.tiles_x * l.marks.tiles_y;
     const int cap = knob > 0 ? knob : st.ctas;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (sh.tab_smem && a.same_box)
-        k5_window_kernel<K, true, true><<<(unsigned)blocks, kWarps * 32, sh.smem, stream>>>(a);
+    if (sh.tab_smem && same_box(l.t))
+        k5_window_kernel<K, true, true><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a);
     else if (sh.tab_smem)
-        k5_window_kernel<K, true, false><<<(unsigned)blocks, kWarps * 32, sh.smem, stream>>>(a);
+        k5_window_kernel<K, true, false><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a);
     else
-        k5_window_kernel<K, false, false><<<(unsigned)blocks, kWarps * 32, sh.smem, stream>>>(a);
+        k5_window_kernel<K, false, false><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -530,9 +480,8 @@ int k_index(int chunk_k) { return chunk_k == 2 ? 0 : (chunk_k == 4 ? 1 : (chunk_
 
 } // namespace
 
-// The window kernel keeps one 64-bit word per region column (4 + 2*hh rows), packs region
-// coordinates into 9 + 6 bits and holds one shared-memory region per warp; larger fields take the
-// chunked gather of sfc_k5_writeback.cu.
+// The window kernel keeps one 64-bit word per region column (8 + 2*hh rows) and packs region
+// coordinates into 9 + 6 bits; larger fields take the chunked gather of sfc_k5_writeback.cu.
 bool k5_window_supported(const TablesDev& t) {
     if (kMarkTileH + 2 * t.max_hh > 64 || kMarkTileW + 2 * t.max_hw > 512) return false;
     return win_shape(t, kEvlMax).smem <= 220 * 1024;

@@ -77,6 +77,7 @@ struct K5Args {
     int ev_max;       // scatter handles tiles with at most this many events in reach
     int debug_stop;   // profiling only (results invalid): leave the scatter kernel after phase N
     int n_tiles;      // tiles_x * tiles_y
+    TileMarks marks;  // scatter kernel: active-tile list written by k-4 (epoch == nullptr: every tile)
 };
 
 struct Smem {
@@ -593,9 +594,26 @@ __global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
             __syncthreads();
         }
     } else if constexpr (MODE == kModeScatter) { // persistent: a CTA strides over the tiles
-        for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-            process_tile<K, SG, ROWS, NT, MODE>(a, sm, tile);
-            __syncthreads();
+        if (a.marks.epoch != nullptr) { // ... over the tiles within reach of this tick's movers (TileMarks)
+            const int n_edge = tile_edge_count(a.marks);
+            const int n_items = n_edge + a.ctl->active_count;
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+                int tile;
+                if (item < n_edge) { // slab mode: tiles whose region reaches the halo rows
+                    const int r = item / a.tiles_x;
+                    const int ty = r < a.marks.edge_lo ? r : a.marks.edge_hi + (r - a.marks.edge_lo);
+                    tile = ty * a.tiles_x + (item - r * a.tiles_x);
+                } else {
+                    tile = a.marks.list[item - n_edge];
+                }
+                process_tile<K, SG, ROWS, NT, MODE>(a, sm, tile);
+                __syncthreads();
+            }
+        } else {
+            for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+                process_tile<K, SG, ROWS, NT, MODE>(a, sm, tile);
+                __syncthreads();
+            }
         }
     } else {
         process_tile<K, SG, ROWS, NT, MODE>(a, sm, blockIdx.x);
@@ -648,6 +666,7 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     a.tab_smem = sh.tab_smem;
     a.part_doubles = sh.part_doubles;
     a.ev_max = l.ev_max;
+    a.marks = (MODE == kModeScatter && kBlockH * ROWS == kMarkTileH) ? l.marks : TileMarks{};
     {
         static const int stop = std::getenv("SFC_K5_DEBUG_STOP") ? std::atoi(std::getenv("SFC_K5_DEBUG_STOP")) : 0;
         a.debug_stop = stop;
@@ -657,6 +676,7 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     a.n_tiles = (int)blocks;
     if (MODE == kModeDense && blocks > l.persistent_ctas) blocks = l.persistent_ctas;
     if (MODE == kModeScatter && blocks > l.scatter_ctas) blocks = l.scatter_ctas;
+    if (MODE == kModeScatter && a.marks.epoch != nullptr && blocks > 4ll * l.persistent_ctas) blocks = 4ll * l.persistent_ctas;
     k5_writeback_kernel<K, SG, ROWS, NT, MODE><<<(unsigned)blocks, NT, sh.smem, stream>>>(a);
     return cudaGetLastError();
 }
@@ -694,10 +714,10 @@ cudaError_t prepare_k(const TablesDev& t) {
 template <int K, int SG>
 cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
     if (l.window_path && k5_window_supported(l.t) && l.dense_list != nullptr) {
-        // window kernel over the active tiles; it hands dense tiles (32 x 4) to the gather kernel
+        // window kernel over the active tiles; it hands dense tiles (32 x 8) to the gather kernel
         const cudaError_t e = launch_k5_window(s, l);
         if (e != cudaSuccess) return e;
-        return launch_one<K, SG, 1, 128, kModeDense>(s, l);
+        return launch_one<K, SG, 2, 128, kModeDense>(s, l);
     }
     if (!two_kernel_path(l.t)) return launch_one<K, SG, 1, 128, kModeAll>(s, l);
     if (l.ev_max <= 0 || l.dense_list == nullptr) return launch_one<K, SG, 2, 128, kModeAll>(s, l);

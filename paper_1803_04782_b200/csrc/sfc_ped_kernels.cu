@@ -380,6 +380,21 @@ __global__ void deinterleave_kernel(const float* __restrict__ dyn, float* __rest
     reinterpret_cast<float4*>(plane)[t] = reinterpret_cast<const float4*>(dyn)[cell * 6 + kind * 2 + half];
 }
 
+// OccupancyGrid of a freshly seeded population (scenario.cpp:424): every su of a footprint holds its
+// pedestrian's id.  Footprints of a valid population are disjoint, so the writes do not collide.
+__global__ void occupancy_from_peds_kernel(GridDev g, PedArrays p, int* __restrict__ occ) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    const int2 c = p.center[i];
+    const uint32_t attr = p.attr[i];
+    const int rw = attr_half_w(attr), rh = attr_half_h(attr);
+    for (int oy = -rh; oy <= rh; ++oy)
+        for (int ox = -rw; ox <= rw; ++ox) {
+            const long long idx = cell_index(g, c.x + ox, c.y + oy);
+            if (idx >= 0) occ[idx] = (int)i;
+        }
+}
+
 __global__ void fill_i8_kernel(int8_t* p, long long n, int v) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = (int8_t)v;
@@ -439,6 +454,11 @@ cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, in
 cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
                                 long long cells) {
     deinterleave_kernel<<<blocks_for(cells * 2, 256), 256, 0, s>>>(dyn + cells_begin * (kKinds * kSects), plane, kind, cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_occupancy_from_peds(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ) {
+    occupancy_from_peds_kernel<<<blocks_for(p.n, 256), 256, 0, s>>>(g, p, occ);
     return cudaGetLastError();
 }
 

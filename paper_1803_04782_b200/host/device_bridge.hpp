@@ -48,6 +48,7 @@ public:
     SlabEngine& operator=(const SlabEngine&) = delete;
 
     void upload(const SimState& s);
+    void seed_resident(const std::vector<Pedestrian>& pedestrians, long tick = 0); // no whole-grid host state
     void download(SimState& s);           // writes the rows and pedestrians this slab owns
     void begin(long ticks);
     void step(int which);                 // 0, 1, 2 — see socfield_cuda.h

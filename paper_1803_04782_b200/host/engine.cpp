@@ -354,6 +354,45 @@ void Engine::download(SimState& s) {
     s.tick = static_cast<long>(v.tick);
 }
 
+namespace {
+// A state view that carries the pedestrians only: sfc_upload then builds the dense buffers on the device.
+sfc_state_view population_view(const std::vector<Pedestrian>& peds, long tick, bridge::PedColumns& cols) {
+    cols.gather(peds);
+    sfc_state_view v{};
+    v.tick = tick;
+    v.n_peds = static_cast<std::int64_t>(peds.size());
+    v.center_xy = cols.center_xy.data();
+    v.walk_period = cols.period.data();
+    v.walk_phase = cols.phase.data();
+    v.goal_sect = cols.goal.data();
+    v.orient_attractive = cols.orient_a.data();
+    v.orient_repulsive = cols.orient_r.data();
+    v.foot_w = cols.foot_w.data();
+    v.foot_h = cols.foot_h.data();
+    return v;
+}
+} // namespace
+
+void Engine::seed_resident(const std::vector<Pedestrian>& pedestrians, long tick) {
+    bridge::PedColumns cols;
+    const sfc_state_view v = population_view(pedestrians, tick, cols);
+    const int status = sfc_upload(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    decisions_.assign(pedestrians.size(), kStill);
+}
+
+std::vector<SuIndex> Engine::download_centers() {
+    std::vector<std::int32_t> xy(2 * decisions_.size());
+    sfc_state_view v{};
+    v.n_peds = static_cast<std::int64_t>(decisions_.size());
+    v.center_xy = xy.data();
+    const int status = sfc_download(dev_, &v);
+    if (status != SFC_OK) throw_status(status);
+    std::vector<SuIndex> out(decisions_.size());
+    for (std::size_t i = 0; i < out.size(); ++i) out[i] = SuIndex{xy[2 * i], xy[2 * i + 1]};
+    return out;
+}
+
 std::vector<TickMetrics> Engine::step_resident(long ticks, bool phase_times) {
     std::vector<TickMetrics> out;
     if (ticks <= 0) return out;
@@ -573,6 +612,24 @@ bool SlabEngine::has_neighbour(int edge) const noexcept {
 void SlabEngine::upload(const SimState& s) {
     PedColumns cols;
     const sfc_state_view v = view_of(const_cast<SimState&>(s), cols);
+    const int status = sfc_upload(h_, &v);
+    if (status != SFC_OK) raise(status);
+}
+
+void SlabEngine::seed_resident(const std::vector<Pedestrian>& pedestrians, long tick) {
+    PedColumns cols;
+    cols.gather(pedestrians);
+    sfc_state_view v{};
+    v.tick = tick;
+    v.n_peds = static_cast<std::int64_t>(pedestrians.size());
+    v.center_xy = cols.center_xy.data();
+    v.walk_period = cols.period.data();
+    v.walk_phase = cols.phase.data();
+    v.goal_sect = cols.goal.data();
+    v.orient_attractive = cols.orient_a.data();
+    v.orient_repulsive = cols.orient_r.data();
+    v.foot_w = cols.foot_w.data();
+    v.foot_h = cols.foot_h.data();
     const int status = sfc_upload(h_, &v);
     if (status != SFC_OK) raise(status);
 }

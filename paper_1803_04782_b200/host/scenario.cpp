@@ -355,15 +355,9 @@ std::vector<SuIndex> draw_centres(const ScenarioConfig& cfg, std::int64_t want, 
 
 } // namespace
 
-SimState seed_population(const ScenarioConfig& cfg) {
+std::vector<Pedestrian> seed_pedestrians(const ScenarioConfig& cfg) {
     validate_scenario(cfg);
     const std::int64_t population = planned_population(cfg);
-
-    SimState state;
-    state.occupancy = OccupancyGrid(cfg.grid);
-    state.static_image = StrengthImage(cfg.grid);
-    state.rng_seed = cfg.seed;
-    state.tick = 0;
 
     std::mt19937_64 rng(cfg.seed);
     const std::vector<SuIndex> centres = draw_centres(cfg, population, rng);
@@ -372,7 +366,8 @@ SimState seed_population(const ScenarioConfig& cfg) {
     std::uniform_int_distribution<int> pick_period(cfg.walk_period_min, cfg.walk_period_max);
     const bool fixed_period = cfg.walk_period_min == cfg.walk_period_max;
 
-    state.pedestrians.reserve(centres.size());
+    std::vector<Pedestrian> pedestrians;
+    pedestrians.reserve(centres.size());
     for (std::size_t i = 0; i < centres.size(); ++i) {
         Pedestrian p;
         p.id = static_cast<std::int32_t>(i);
@@ -384,9 +379,20 @@ SimState seed_population(const ScenarioConfig& cfg) {
         p.dyn_fields = templates;
         for (FieldSpec& f : p.dyn_fields)
             if (is_directional(f.kind)) f.orientation = p.goal_sect;
-        for (const SuIndex su : footprint_cells(cfg.grid, p.center, p.footprint).cells) state.occupancy.set(su, p.id);
-        state.pedestrians.push_back(std::move(p));
+        pedestrians.push_back(std::move(p));
     }
+    return pedestrians;
+}
+
+SimState seed_population(const ScenarioConfig& cfg) {
+    SimState state;
+    state.pedestrians = seed_pedestrians(cfg);
+    state.occupancy = OccupancyGrid(cfg.grid);
+    state.static_image = StrengthImage(cfg.grid);
+    state.rng_seed = cfg.seed;
+    state.tick = 0;
+    for (const Pedestrian& p : state.pedestrians)
+        for (const SuIndex su : footprint_cells(cfg.grid, p.center, p.footprint).cells) state.occupancy.set(su, p.id);
     state.dyn_images = rasterize_dynamic(state.pedestrians, cfg.grid); // device rasteriser
     return state;
 }

@@ -92,7 +92,11 @@ class SlabRunner:
         self.device = torch.device("cuda", device_index)
         ped_half_h = (cfg.pedestrian_geometry[1] - 1) // 2
         self.engine = sf.SlabEngine(cfg, rank, world, ped_half_h, device_index)
-        self.engine.upload(state)
+        if state is None:  # seed on the device: no whole-grid host SimState (32768^2 would need 141 GB per rank)
+            self.population = self.engine.seed_resident(cfg)
+        else:
+            self.engine.upload(state)
+            self.population = state.population
         self.bufs = {}
         for kind in range(4):
             for edge in (0, 1):

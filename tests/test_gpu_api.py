@@ -321,3 +321,30 @@ def test_c2_full_size_properties(product_lib):
     c = gpu.centers()
     assert (occ[c[:, 1], c[:, 0]] == np.arange(20000)).all()
     assert np.abs(gpu.images() - gpu.rebuild_images()).max() < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("text", [
+    "grid = 96x64\ndensity = 0.3\ndirections = eight\nwalk_period = 1..3\nseed = 7\nrebuild_interval = 10\n",
+    "grid = 70x50\nboundary = closed\ndensity = 0.1\ndirections = four\npedestrian_geometry = 3x3\nseed = 3\nrebuild_interval = 0\n",
+])
+def test_seed_resident_equals_host_seeding(text):
+    """Engine.seed_resident (device-built occupancy and images, no host SimState) is bit-identical to
+    upload(seed_population(cfg)) — scenario.cpp:392-429 — right after seeding and after 25 ticks."""
+    cfg = sf.parse_scenario(text)
+    host = sf.seed_population(cfg)
+    a = sf.Engine(cfg)
+    a.upload(host)
+    b = sf.Engine(cfg)
+    assert b.seed_resident(cfg) == host.population
+    out = host.copy()
+    for ticks in (0, 25):
+        if ticks:
+            a.step_resident(ticks)
+            b.step_resident(ticks)
+        a.download(host)
+        b.download(out)
+        assert np.array_equal(b.download_centers(), host.centers())
+        assert np.array_equal(out.occupancy(), host.occupancy())
+        for kind in ("dir-attractive", "dir-repulsive", "recurrent-repulsive"):
+            assert np.array_equal(out.image(kind).view(np.uint32), host.image(kind).view(np.uint32)), kind
