@@ -583,7 +583,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         const TileMarks& m = e->marks_alloc;
         const long long per_mover = (long long)((2 * m.hw + 1) / kMarkTileW + 2) * ((2 * m.hh + 1) / kMarkTileH + 2);
         const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
-        const bool sparse = P * per_mover * 2 < n_tiles;
+        const bool sparse = P * per_mover < 2 * n_tiles; // (expected share of active tiles below ~85 %)
         // sparse crowds: the window kernel (its per-tile cost is the lower one when a tile holds an
         // event or two); otherwise the scatter kernel, which puts a whole CTA on every tile
         const int window = e->k5_window_ok && (e->k5_window_pref == 1 || (e->k5_window_pref < 0 && sparse));

@@ -39,8 +39,9 @@
 // Fields larger than the grid wrap onto themselves (test_engine.cpp:329-340): the region is
 // scanned in unwrapped coordinates, so one physical su can appear several times, once per
 // periodic image — exactly the reference's while-loop wraps (engine.cpp:450-454).
-// Regions too large for shared memory (very large fields) use 32 x 4 tiles, gather only, with the
-// region staged in column chunks: the list is sorted, so chunks arrive in order.
+// Regions too large for shared memory (very large fields) use 32 x 16 tiles, gather only, with the
+// region staged in column chunks: the list is sorted, so chunks arrive in order and are appended to
+// one list as long as the events fit (else the walks re-stage chunk by chunk).
 
 #include <cstdlib>
 
@@ -134,25 +135,48 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
     // Stages the event codes of region columns [c0, c1) in shared memory (coalesced row reads,
     // column-major store), then compacts the non-zero ones into evl ordered by (x, y).
     // Returns the event count (uniform across the CTA).
-    auto build_list = [&](int c0, int c1) -> int {
+    // With base >= 0 the events are APPENDED at evl[base..] and colstart is indexed by region column
+    // (chunks arrive in column order, so the list stays sorted); returns -1, writing nothing, when
+    // the list would overflow.
+    auto build_list = [&](int c0, int c1, int base = -1) -> int {
         const int ncols = c1 - c0;
+        const bool append = base >= 0;
+        int* const cs = append ? colstart + c0 : colstart; // cs[rc] .. cs[rc + 1]: events of column c0 + rc
         const bool narrow = RW <= g.W; // one conditional add wraps x (wider regions take the general path)
-        for (int ry = warp; ry < RH; ry += NW) {
-            const long long row = cell_index(g, 0, ys + ry); // uniform per warp; -1: row does not exist
-            for (int rc = lane; rc < ncols; rc += 32) {
-                int x = xs + c0 + rc;
-                long long idx = -1;
-                if (narrow) {
-                    if (g.closed) {
-                        if (row >= 0 && x >= 0 && x < g.W) idx = row + x;
-                    } else if (row >= 0) {
-                        x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
-                        idx = row + x;
+        { // row-major over the chunk (coalesced), eight loads of a thread in flight before the first use
+            const int n_cells = ncols * RH;
+            const unsigned inv_cols = 0xFFFFFFFFu / (unsigned)ncols + 1u;
+            for (int i0 = 0; i0 < n_cells; i0 += 8 * NT) {
+                uint16_t got[8];
+                int at[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = i0 + q * NT + tid;
+                    got[q] = 0;
+                    at[q] = -1;
+                    if (i < n_cells) {
+                        const int ry = (int)__umulhi((unsigned)i, inv_cols); // i / ncols
+                        const int rc = i - ry * ncols;
+                        at[q] = rc * RH + ry;
+                        int x = xs + c0 + rc;
+                        long long idx = -1;
+                        if (narrow) {
+                            const long long row = cell_index(g, 0, ys + ry); // -1: row does not exist
+                            if (g.closed) {
+                                if (row >= 0 && x >= 0 && x < g.W) idx = row + x;
+                            } else if (row >= 0) {
+                                x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
+                                idx = row + x;
+                            }
+                        } else {
+                            idx = cell_index(g, x, ys + ry);
+                        }
+                        if (idx >= 0) got[q] = __ldg(ev16 + idx);
                     }
-                } else {
-                    idx = cell_index(g, x, ys + ry);
                 }
-                codes[rc * RH + ry] = idx >= 0 ? __ldg(ev16 + idx) : (uint16_t)0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (at[q] >= 0) codes[at[q]] = got[q];
             }
         }
         __syncthreads();
@@ -162,28 +186,29 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
                 const int ry = r0 + lane;
                 cnt += __popc(__ballot_sync(0xFFFFFFFFu, ry < RH && codes[rc * RH + ry] != 0));
             }
-            if (lane == 0) colstart[rc + 1] = cnt;
+            if (lane == 0) cs[rc + 1] = cnt;
         }
-        if (tid == 0) colstart[0] = 0;
+        if (tid == 0) cs[0] = append ? base : 0;
         __syncthreads();
         if (warp == 0) { // inclusive scan of the shifted counts = exclusive column starts
-            int carry = 0;
-            for (int base = 1; base <= ncols; base += 32) {
-                const int i = base + lane;
-                int v = i <= ncols ? colstart[i] : 0;
+            int carry = append ? base : 0;
+            for (int b1 = 1; b1 <= ncols; b1 += 32) {
+                const int i = b1 + lane;
+                int v = i <= ncols ? cs[i] : 0;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
                     if (lane >= o) v += u;
                 }
-                if (i <= ncols) colstart[i] = v + carry;
+                if (i <= ncols) cs[i] = v + carry;
                 carry += __shfl_sync(0xFFFFFFFFu, v, 31);
             }
         }
         __syncthreads();
+        if (append && cs[ncols] > a.cap) return -1; // uniform
         for (int rc = warp; rc < ncols; rc += NW) {
-            int pos = colstart[rc];
-            if (colstart[rc + 1] == pos) continue;
+            int pos = cs[rc];
+            if (cs[rc + 1] == pos) continue;
             for (int r0 = 0; r0 < RH; r0 += 32) {
                 const int ry = r0 + lane;
                 const uint32_t code = ry < RH ? codes[rc * RH + ry] : 0u;
@@ -194,10 +219,11 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             }
         }
         __syncthreads();
-        return colstart[ncols];
+        return cs[ncols] - (append ? base : 0);
     };
 
     int n_events = 0;
+    bool one_list = single_pass; // the whole region's events sit in evl, colstart spans the region
     if constexpr (MODE == kModeScatter) {
         // The scatter does not need the events in order (only its rare exact replays do), so the
         // region is read straight from the event map — rows on warps, columns on lanes — and the
@@ -270,6 +296,22 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
     } else if (single_pass) {
         n_events = build_list(0, RW);
         if (n_events == 0) return; // nobody moved within reach of this tile
+    } else { // large field: stage the region chunk by chunk, keep ONE list if the events fit
+        int total = 0;
+        one_list = true;
+        for (int c0 = 0; c0 < RW; c0 += cols_per_pass) {
+            const int n = build_list(c0, min(RW, c0 + cols_per_pass), total);
+            __syncthreads();
+            if (n < 0) {
+                one_list = false;
+                break;
+            }
+            total += n;
+        }
+        if (one_list) {
+            n_events = total;
+            if (n_events == 0) return;
+        }
     }
 
     // =========================================================================================
@@ -504,7 +546,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             const int blk = b0 + warp;
             const int bx = (blk % 4) * kBlockW, by = (blk / 4) * kBlockH;
             const bool blk_ok = blk < NBLK && by < ny && bx < nx; // uniform per warp
-            if (single_pass && !blk_ok) continue; // (chunked mode keeps every warp in the CTA-wide list builds)
+            if (one_list && !blk_ok) continue; // (chunked mode keeps every warp in the CTA-wide list builds)
             const int cx = bx + (lane % kBlockW), cy = by + (lane / kBlockW); // my su in the tile
             const int tcx = cx + HW, tcy = cy + HH;                             // ... in region coordinates
             const bool in_grid = blk_ok && cx < nx && cy < ny;
@@ -512,7 +554,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             float4* rec = reinterpret_cast<float4*>(a.dyn + (cell < 0 ? 0 : cell) * 24);
             // events that can reach the block lie in a contiguous range of the x-sorted list
             int e_lo = 0, e_hi = n_events;
-            if (single_pass) {
+            if (one_list) {
                 e_lo = colstart[max(bx, 0)];
                 e_hi = colstart[min(bx + kBlockW + 2 * HW, RW)];
                 if (e_lo == e_hi) continue; // uniform
@@ -528,7 +570,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
 #pragma unroll 1
                 for (int sg = 0; sg < NG; ++sg) {
                     unsigned long long dirty = 0ull;
-                    if (single_pass) {
+                    if (one_list) {
                         if (in_grid) walk(e_lo, e_hi, kind, sg, kt, kmag, kinfo, tcx, tcy, by + HH, dirty);
                     } else { // chunked region: the list is rebuilt per (kind, group)
                         for (int c0 = 0; c0 < RW; c0 += cols_per_pass) {
@@ -694,7 +736,7 @@ cudaError_t prepare_one(const TablesDev& t) {
 }
 
 // Small fields (the whole 32 x 8 tile region is staged at once, tables in shared memory): scatter
-// + dense gather.  Otherwise 32 x 4 tiles, gather only, chunked staging.
+// + dense gather.  Otherwise 32 x 16 tiles, gather only, chunked staging.
 bool two_kernel_path(const TablesDev& t) {
     return (kTileW + 2 * t.max_hw) * (kBlockH * 2 + 2 * t.max_hh) <= kChunkCells && t.total_entries <= kTabSmemMax &&
            (2 * t.max_hw + 1) * (2 * t.max_hh + 1) <= kOboxMax && t.max_hw < 128 && t.max_hh < 128;
@@ -708,6 +750,7 @@ cudaError_t prepare_k(const TablesDev& t) {
     if (e == cudaSuccess) e = prepare_one<K, SG, 1, 128, kModeDense>(t);
     if (e == cudaSuccess) e = prepare_one<K, SG, 2, 128, kModeAll>(t);
     if (e == cudaSuccess) e = prepare_one<K, SG, 1, 128, kModeAll>(t);
+    if (e == cudaSuccess) e = prepare_one<K, SG, 4, 128, kModeAll>(t);
     return e;
 }
 
@@ -719,7 +762,8 @@ cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
         if (e != cudaSuccess) return e;
         return launch_one<K, SG, 2, 128, kModeDense>(s, l);
     }
-    if (!two_kernel_path(l.t)) return launch_one<K, SG, 1, 128, kModeAll>(s, l);
+    // large fields: 32 x 16 tiles (the field halo is staged once per 512 su), gather only
+    if (!two_kernel_path(l.t)) return launch_one<K, SG, 4, 128, kModeAll>(s, l);
     if (l.ev_max <= 0 || l.dense_list == nullptr) return launch_one<K, SG, 2, 128, kModeAll>(s, l);
     if (l.tile_rows == 4) { // 32 x 4 tiles: less shared memory per CTA, more CTAs per SM
         const cudaError_t e = launch_one<K, SG, 1, 256, kModeScatter>(s, l);

@@ -67,5 +67,9 @@ EXTRA = {
                "field_decay = -0.37\nwalk_period = 1..4\nseed = 17\nrebuild_interval = 6\n",
     "ped5": "grid = 64x48\ndensity = 0.35\ndirections = eight\npedestrian_geometry = 5x3\nfield_geometry = 9x9\n"
             "walk_period = 1..2\nseed = 4\nrebuild_interval = 8\n",
+    # sparse crowds on ragged grids: most k-5 tiles see no mover in a tick (active-tile list, wrap-around marking)
+    "sparse-periodic": "grid = 203x117\ndensity = 0.004\ndirections = eight\nwalk_period = 1..2\nseed = 61\nrebuild_interval = 12\n",
+    "sparse-closed": "grid = 150x90\nboundary = closed\ndensity = 0.006\ndirections = four\nseed = 62\nrebuild_interval = 9\n",
+    "sparse-field15": "grid = 160x96\ndensity = 0.003\ndirections = eight\nfield_geometry = 15x11\nseed = 63\nrebuild_interval = 0\n",
     "wide-ragged": "grid = 131x67\ndensity = 0.3\ndirections = bi\nwalk_period = 1..3\nseed = 123\nrebuild_interval = 10\n",
 }

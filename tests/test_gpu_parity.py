@@ -142,3 +142,28 @@ def test_both_k5_formulations(product_lib, monkeypatch, name, knob):
     for step in range(4):
         np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
         assert_state_equal(gpu, cpu, f"{name} knob {knob} tick {8 * (step + 1)}")
+
+
+@pytest.mark.parametrize("path,knob", [("window", None), ("window", "100000"), ("window", "2"), ("scatter-list", None)])
+@pytest.mark.parametrize("name", ["desk64", "k2", "k16", "field-5x9", "field21", "field-bigger-than-grid", "closed-four",
+                                  "closed-ped3", "ped5", "wide-ragged", "sparse-periodic", "sparse-closed", "sparse-field15",
+                                  "d0.9-four-ped3"])
+def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path, knob):
+    """k-4 lists the 32 x 8 tiles within field reach of a mover and k-5 visits only those; sparse
+    crowds also switch to the window kernel (one warp per 8 x 4 su block, event-major scatter, exact
+    replay).  Forced here on crowds of every density: the window kernel with its default hand-off
+    to the dense gather, with every tile kept (knob 100000) or nearly every tile handed off (2), and
+    the scatter kernel driven from the list.  All bit-identical to the oracle."""
+    if path == "window":
+        monkeypatch.setenv("SFC_K5_PATH", "window")
+    else:
+        monkeypatch.setenv("SFC_K5_PATH", "scatter")
+        monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "1")
+    if knob is not None:
+        monkeypatch.setenv("SFC_K5_EVENT_MAX", knob)
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(4):
+        np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} {path} knob {knob} tick {8 * (step + 1)}")

@@ -38,6 +38,27 @@ def test_slabs_equal_undivided_grid(product_lib, monkeypatch, name, slabs):
     gpu.verify()
 
 
+@pytest.mark.parametrize("name,slabs", [("desk64", 2), ("closed-four", 2), ("wide-ragged", 3), ("field21", 2),
+                                        ("sparse-periodic", 3), ("sparse-closed", 2), ("sparse-field15", 2)])
+@pytest.mark.parametrize("path", ["window", "scatter-list"])
+def test_slabs_with_active_tile_list(product_lib, monkeypatch, name, slabs, path):
+    """Slabs keep the tiles whose field region reaches into the halo rows permanently active (the
+    neighbours' events arrive there as row copies, unseen by this slab's k-4) and list the rest."""
+    monkeypatch.setenv("SFC_SLABS", str(slabs))
+    monkeypatch.setenv("SFC_K5_PATH", "window" if path == "window" else "scatter")
+    if path != "window":
+        monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "1")
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for chunk in (1, 7, 22):
+        np.testing.assert_array_equal(gpu.run(chunk), cpu.run(chunk), err_msg=f"{name} x{slabs} moved")
+        np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"{name} x{slabs} tick {gpu.tick} centres")
+        np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"{name} x{slabs} tick {gpu.tick} occupancy")
+        for k in range(3):
+            np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)), err_msg=f"{name} x{slabs} image {k}")
+
+
 def test_slab_halo_too_thin_is_a_config_error(product_lib, monkeypatch):
     monkeypatch.setenv("SFC_SLABS", "8")  # 24 rows / 8 = 3 owned rows < halo 4
     gpu = shim.Sim.from_scenario(product_lib, sc.SEQPAR24)
@@ -48,7 +69,7 @@ def test_slab_halo_too_thin_is_a_config_error(product_lib, monkeypatch):
 
 # ---- the multi-process path: one rank per slab, torch.distributed halo exchange ---------------
 
-def _rank_main(rank, world, port, text, ticks, out):
+def _rank_main(rank, world, port, text, ticks, out, seed_on_device=False):
     import os
 
     import torch.distributed as dist
@@ -61,7 +82,10 @@ def _rank_main(rank, world, port, text, ticks, out):
     try:
         cfg = sf.parse_scenario(text)
         state = sf.seed_population(cfg)
-        runner = slabs.SlabRunner(sf, cfg, state, dist, rank, world, 0)
+        # seed_on_device: the slab builds its occupancy rows and images itself (no whole-grid host state);
+        # `state` is then only the download target of this test
+        runner = slabs.SlabRunner(sf, cfg, None if seed_on_device else state, dist, rank, world, 0)
+        assert runner.population == state.population
         moved = runner.run(ticks)
         runner.download(state)  # this rank's rows and pedestrians only
         eng = runner.engine
@@ -73,8 +97,10 @@ def _rank_main(rank, world, port, text, ticks, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("desk64", 2), ("closed-four", 2), ("linear-regulation", 3)])
-def test_multi_process_slabs(name, world):
+@pytest.mark.parametrize("name,world,seed_on_device", [("desk64", 2, False), ("closed-four", 2, False),
+                                                       ("linear-regulation", 3, False), ("desk64", 2, True),
+                                                       ("sparse-periodic", 3, True)])
+def test_multi_process_slabs(name, world, seed_on_device):
     import socket
 
     import torch.multiprocessing as mp
@@ -86,7 +112,7 @@ def test_multi_process_slabs(name, world):
         port = s.getsockname()[1]
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_rank_main, args=(world, port, text, ticks, out), nprocs=world, join=True)
+    mp.spawn(_rank_main, args=(world, port, text, ticks, out, seed_on_device), nprocs=world, join=True)
     cpu = oracle.OracleSim.from_scenario(text)
     moved = cpu.run(ticks)
     total = np.sum([np.array(out[r]["moved"]) for r in range(world)], axis=0)
