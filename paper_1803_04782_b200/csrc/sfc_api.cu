@@ -9,12 +9,29 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <atomic>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sfc_internal.cuh"
 
 using namespace sfc;
+
+// Host <-> device bulk copies of the caller's pageable SimState buffers (std::vector storage):
+// several host threads each move their slice through their own pair of pinned buffers and their
+// own stream, so the CPU memcpy into pinned memory and the PCIe DMA overlap and add up across
+// lanes (a single cudaMemcpy from pageable memory is bound by one core's memcpy).
+struct Stager {
+    static constexpr int kLanes = 4;
+    static constexpr size_t kChunk = 4u << 20;
+    void* pin[kLanes][2] = {};
+    bool busy[kLanes][2] = {};
+    cudaStream_t st[kLanes] = {};
+    cudaEvent_t ev[kLanes][2] = {};
+    cudaEvent_t fence = nullptr;
+    bool ready = false;
+};
 
 struct sfc_engine {
     sfc_config cfg{};
@@ -63,6 +80,7 @@ struct sfc_engine {
     TileMarks marks_alloc{}; // ... the allocation (the list is only switched on for sparse crowds, see sfc_upload)
     int k5_active_list = -1; // SFC_K5_ACTIVE_LIST: 0 never, 1 always, -1 by crowd density
     int sm_count = 148;
+    Stager stager;
     bool uploaded = false;
     long long tick = 0;
     sfc_counters counters{};
@@ -172,6 +190,109 @@ int ensure_stage(sfc_engine* e) {
     return SFC_OK;
 }
 
+bool stager_init(sfc_engine* e) {
+    Stager& s = e->stager;
+    if (s.ready) return true;
+    if (std::getenv("SFC_NO_STAGER")) return false;
+    bool ok = cudaEventCreateWithFlags(&s.fence, cudaEventDisableTiming) == cudaSuccess;
+    for (int t = 0; t < Stager::kLanes && ok; ++t) {
+        ok = cudaStreamCreateWithFlags(&s.st[t], cudaStreamNonBlocking) == cudaSuccess;
+        for (int b = 0; b < 2 && ok; ++b)
+            ok = cudaHostAlloc(&s.pin[t][b], Stager::kChunk, cudaHostAllocDefault) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&s.ev[t][b], cudaEventDisableTiming) == cudaSuccess;
+    }
+    s.ready = ok;
+    return ok;
+}
+
+void stager_destroy(sfc_engine* e) {
+    Stager& s = e->stager;
+    for (int t = 0; t < Stager::kLanes; ++t) {
+        if (s.st[t]) cudaStreamSynchronize(s.st[t]);
+        for (int b = 0; b < 2; ++b) {
+            if (s.pin[t][b]) cudaFreeHost(s.pin[t][b]);
+            if (s.ev[t][b]) cudaEventDestroy(s.ev[t][b]);
+        }
+        if (s.st[t]) cudaStreamDestroy(s.st[t]);
+    }
+    if (s.fence) cudaEventDestroy(s.fence);
+    s = Stager{};
+}
+
+// Copies `bytes` between a pageable host buffer and device memory, ordered like a copy enqueued on
+// the engine's stream.  to_device: the host buffer may be reused on return and later work on the
+// engine's stream sees the data.  Otherwise the host buffer holds the data on return.
+cudaError_t bulk_copy(sfc_engine* e, void* dev, void* host, size_t bytes, bool to_device) {
+    if (bytes < (1u << 20) || !stager_init(e)) {
+        cudaError_t c = to_device ? cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, e->stream)
+                                  : cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, e->stream);
+        if (c == cudaSuccess && !to_device) c = cudaStreamSynchronize(e->stream);
+        return c;
+    }
+    Stager& s = e->stager;
+    cudaError_t c = cudaEventRecord(s.fence, e->stream); // the lanes start after what the engine's stream holds so far
+    if (c != cudaSuccess) return c;
+    std::atomic<int> err{(int)cudaSuccess};
+    const size_t per_lane = ((bytes + Stager::kLanes - 1) / Stager::kLanes + 255) & ~(size_t)255;
+    auto lane = [&](int t) {
+        auto check = [&](cudaError_t r) {
+            if (r != cudaSuccess) {
+                int none = (int)cudaSuccess;
+                err.compare_exchange_strong(none, (int)r);
+            }
+            return r == cudaSuccess;
+        };
+        if (!check(cudaSetDevice(e->device)) || !check(cudaStreamWaitEvent(s.st[t], s.fence, 0))) return;
+        const size_t begin = std::min(bytes, per_lane * t), end = std::min(bytes, per_lane * (t + 1));
+        char* const d = static_cast<char*>(dev);
+        char* const h = static_cast<char*>(host);
+        size_t prev_off = 0, prev_n = 0;
+        int prev_b = -1, i = 0;
+        for (size_t off = begin; off < end; off += Stager::kChunk, ++i) {
+            const int b = i & 1;
+            const size_t n = std::min(Stager::kChunk, end - off);
+            if (s.busy[t][b] && !check(cudaEventSynchronize(s.ev[t][b]))) return; // the buffer's last DMA is done
+            if (to_device) {
+                std::memcpy(s.pin[t][b], h + off, n);
+                if (!check(cudaMemcpyAsync(d + off, s.pin[t][b], n, cudaMemcpyHostToDevice, s.st[t]))) return;
+            } else {
+                if (!check(cudaMemcpyAsync(s.pin[t][b], d + off, n, cudaMemcpyDeviceToHost, s.st[t]))) return;
+            }
+            if (!check(cudaEventRecord(s.ev[t][b], s.st[t]))) return;
+            s.busy[t][b] = true;
+            if (!to_device) { // drain the previous chunk while this one is in flight
+                if (prev_b >= 0) {
+                    if (!check(cudaEventSynchronize(s.ev[t][prev_b]))) return;
+                    std::memcpy(h + prev_off, s.pin[t][prev_b], prev_n);
+                    s.busy[t][prev_b] = false;
+                }
+                prev_b = b;
+                prev_off = off;
+                prev_n = n;
+            }
+        }
+        if (!to_device && prev_b >= 0) {
+            if (!check(cudaEventSynchronize(s.ev[t][prev_b]))) return;
+            std::memcpy(h + prev_off, s.pin[t][prev_b], prev_n);
+            s.busy[t][prev_b] = false;
+        }
+    };
+    std::thread workers[Stager::kLanes - 1];
+    for (int t = 1; t < Stager::kLanes; ++t) workers[t - 1] = std::thread(lane, t);
+    lane(0);
+    for (auto& w : workers) w.join();
+    if (err.load() != (int)cudaSuccess) return (cudaError_t)err.load();
+    if (to_device) { // later work on the engine's stream waits for every lane's DMA
+        for (int t = 0; t < Stager::kLanes; ++t)
+            for (int b = 0; b < 2; ++b)
+                if (s.busy[t][b]) {
+                    c = cudaStreamWaitEvent(e->stream, s.ev[t][b], 0);
+                    if (c != cudaSuccess) return c;
+                }
+    }
+    return cudaSuccess;
+}
+
 // Contiguous runs of resident rows: (first global row, first local row, row count).  The whole-grid
 // engine has one; a slab has its owned rows plus up to two halo runs per side (periodic wrap) or
 // fewer (closed boundary: rows beyond the grid do not exist and keep their "empty" initial value).
@@ -265,6 +386,15 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.marks = e->marks;
     l.window_path = e->k5_window;
     return l;
+}
+
+// Tile stamps repeat with period kEpochPeriod: erase them once per period so that a stamp left by
+// a tick exactly one period ago cannot pass for the current one.
+int erase_marks_if_due(sfc_engine* e, long long tick) {
+    if (e->marks_alloc.epoch && tick > 0 && tick % (long long)kEpochPeriod == 0)
+        SFC_CUDA(cudaMemsetAsync(e->marks_alloc.epoch, 0,
+                                 sizeof(unsigned) * (size_t)e->marks_alloc.tiles_x * e->marks_alloc.tiles_y, e->stream));
+    return SFC_OK;
 }
 
 int enqueue_tick_kernels(sfc_engine* e) {
@@ -414,7 +544,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
         cu(dev_alloc(&m.epoch, n_tiles), "cudaMalloc(tile epochs)");
         cu(dev_alloc(&m.list, n_tiles), "cudaMalloc(active tile list)");
-        if (rc == SFC_OK) cu(cudaMemset(m.epoch, 0, sizeof(int) * (size_t)n_tiles), "cudaMemset");
+        if (rc == SFC_OK) cu(cudaMemset(m.epoch, 0, sizeof(unsigned) * (size_t)n_tiles), "cudaMemset");
         // events per tile region above which nearly every address needs the exact K-slot walk:
         // about 4.5 events per field window
         const long long region = (long long)(kMarkTileW + 2 * m.hw) * (kMarkTileH + 2 * m.hh);
@@ -477,6 +607,7 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->ev);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
+    stager_destroy(e);
     cudaFree(e->marks_alloc.epoch);
     cudaFree(e->marks_alloc.list);
     for (int edge = 0; edge < 2; ++edge)
@@ -538,20 +669,18 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
     for (const RowSeg& seg : row_segments(e, false)) { // the host arrays cover the whole grid
         const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
         if (v->occupancy) {
-            SFC_CUDA(cudaMemcpyAsync(e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, cudaMemcpyHostToDevice, e->stream));
+            SFC_CUDA(bulk_copy(e, e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, true));
             e->counters.h2d_bytes += (int64_t)(sizeof(int) * n_seg);
         }
         if (v->static_image) {
-            SFC_CUDA(cudaMemcpyAsync(e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects,
-                                     cudaMemcpyHostToDevice, e->stream));
+            SFC_CUDA(bulk_copy(e, e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects, true));
             e->counters.h2d_bytes += (int64_t)(sizeof(float) * n_seg * kSects);
         }
         for (int k = 0; k < kKinds; ++k) {
             if (!v->dyn_images[k]) continue;
             for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
                 const long long n = std::min(e->stage_cells, n_seg - c0);
-                SFC_CUDA(cudaMemcpyAsync(e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects,
-                                         cudaMemcpyHostToDevice, e->stream));
+                SFC_CUDA(bulk_copy(e, e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects, true));
                 SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, dc + c0, n));
                 e->counters.kernel_launches += 1;
                 e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
@@ -595,7 +724,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
             e->graph_valid = false;
         }
         // the tick counter may restart: forget every epoch stamp
-        SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(int) * (size_t)n_tiles, e->stream));
+        SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(unsigned) * (size_t)n_tiles, e->stream));
     }
     Ctl h{};
     h.tick = v->tick;
@@ -626,7 +755,7 @@ int sfc_download(sfc_engine* e, sfc_state_view* v) {
     for (const RowSeg& seg : row_segments(e, true)) { // only the rows this engine owns are authoritative
         const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
         if (v->occupancy) {
-            SFC_CUDA(cudaMemcpyAsync(v->occupancy + hc, e->occ + dc, sizeof(int) * (size_t)n_seg, cudaMemcpyDeviceToHost, e->stream));
+            SFC_CUDA(bulk_copy(e, e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, false));
             e->counters.d2h_bytes += (int64_t)(sizeof(int) * n_seg);
         }
         for (int k = 0; k < kKinds; ++k) {
@@ -634,16 +763,14 @@ int sfc_download(sfc_engine* e, sfc_state_view* v) {
             for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
                 const long long n = std::min(e->stage_cells, n_seg - c0);
                 SFC_CUDA(launch_deinterleave(e->stream, e->dyn, e->stage, k, dc + c0, n));
-                SFC_CUDA(cudaMemcpyAsync(v->dyn_images[k] + (hc + c0) * kSects, e->stage, sizeof(float) * (size_t)n * kSects,
-                                         cudaMemcpyDeviceToHost, e->stream));
-                SFC_CUDA(cudaStreamSynchronize(e->stream)); // staging buffer is reused by the next chunk
+                // (returns with the data on the host: the staging buffer is free for the next chunk)
+                SFC_CUDA(bulk_copy(e, e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects, false));
                 e->counters.kernel_launches += 1;
                 e->counters.d2h_bytes += (int64_t)(sizeof(float) * n * kSects);
             }
         }
         if (v->static_image) {
-            SFC_CUDA(cudaMemcpyAsync(v->static_image + hc * kSects, e->stat + dc * kSects, sizeof(float) * (size_t)n_seg * kSects,
-                                     cudaMemcpyDeviceToHost, e->stream));
+            SFC_CUDA(bulk_copy(e, e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects, false));
             e->counters.d2h_bytes += (int64_t)(sizeof(float) * n_seg * kSects);
         }
     }
@@ -690,6 +817,8 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
     }
     SFC_CUDA(cudaEventRecord(e->ev_start, e->stream));
     for (long long t = 0; t < ticks; ++t) {
+        rc = erase_marks_if_due(e, base + t);
+        if (rc != SFC_OK) return rc;
         if (with_phase_times) {
             const DebugArrays none{};
             cudaEvent_t* ev = &evs[(size_t)t * 5];
@@ -768,6 +897,8 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
             e->counters.kernel_launches += 2;
             break;
         case 3:
+            rc = erase_marks_if_due(e, e->tick);
+            if (rc != SFC_OK) return rc;
             SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
             SFC_CUDA(launch_dbg_vote(e->stream, e->dbg, e->dp.fault_invert));
             e->counters.kernel_launches += 2;
@@ -927,7 +1058,10 @@ int sfc_slab_step(sfc_engine* e, int step) {
                 SFC_CUDA(launch_halo_pack(e->stream, e->g, e->peds, e->ctl, edge, 0, depth, e->halo_send[edge][0], e->halo_capacity));
             e->counters.kernel_launches += 7;
             break;
-        case 1: // adopt the neighbours' decisions, vote, move, publish the positions of my boundary pedestrians
+        case 1: { // adopt the neighbours' decisions, vote, move, publish the positions of my boundary pedestrians
+            const int rc = erase_marks_if_due(e, e->tick);
+            if (rc != SFC_OK) return rc;
+        }
             for (int edge = 0; edge < 2; ++edge)
                 if (slab_has_neighbour(e, edge))
                     SFC_CUDA(launch_halo_unpack(e->stream, e->peds, e->ctl, 0, e->halo_recv[edge][0], e->halo_capacity));

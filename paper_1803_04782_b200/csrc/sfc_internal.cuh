@@ -133,6 +133,7 @@ struct Ctl {
     int ev_written_count;    // slab mode: entries of SlabDev::ev_written
     int halo_counts[4];      // slab mode: records packed per (edge, kind): [edge*2 + kind]
     int active_count;        // k-5: tiles within reach of this tick's movers (TileMarks::list), reset by k-3
+    unsigned int epoch;      // k-5: this tick's tile stamp (set by k-3, read by k-4 and k-5; never 0)
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -176,8 +177,10 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, int code, int phase, int x
 // In slab mode the tiles whose field region reaches into the halo rows ("edge tiles") are not
 // listed — the neighbours' events arrive there as plain row copies — and are always processed.
 constexpr int kMarkTileW = 32, kMarkTileH = 8;
+constexpr unsigned kEpochPeriod = (1u << 20) - 1u; // stamps are erased once per period (sfc_run)
+constexpr unsigned kMarkCountMax = 0xFFFu;
 struct TileMarks {
-    int* epoch;      // [tiles_x * tiles_y] last epoch (tick + 1) the tile was listed in
+    unsigned* epoch; // [tiles_x * tiles_y] stamp << 12 | movers within reach (saturating), stamp = tick % period + 1
     int* list;       // [tiles_x * tiles_y]
     int tiles_x, tiles_y;
     int hw, hh;      // field reach (largest half extents over the three kinds)

@@ -161,7 +161,10 @@ k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const floa
 __global__ void __launch_bounds__(kPedThreads)
 k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault, SlabDev slab) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) ctl->active_count = 0; // k-4 rebuilds the active-tile list of k-5 every tick
+    if (i == 0) { // k-4 rebuilds the active-tile list of k-5 every tick
+        ctl->active_count = 0;
+        ctl->epoch = (unsigned)(ctl->tick % kEpochPeriod) + 1u;
+    }
     if (i >= p.n) return;
     if (ctl->error_code != 0) return;
     const int d = p.dir[i];
@@ -216,7 +219,7 @@ __device__ __forceinline__ int wrapped_intervals(int lo, int hi, int n, bool clo
 }
 
 // Lists every k-5 tile within field reach of a mover's old or new centre (TileMarks).
-__device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m, Ctl* ctl, int epoch, int fx, int fy, int ux,
+__device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m, Ctl* ctl, unsigned epoch, int fx, int fy, int ux,
                                            int uy, bool slab_active) {
     int xr[2][2], yr[2][2];
     const int nxr = wrapped_intervals(min(fx, fx + ux) - m.hw, max(fx, fx + ux) + m.hw, g.W, g.closed != 0, 0, g.W, xr);
@@ -227,8 +230,18 @@ __device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m,
             for (int ix = 0; ix < nxr; ++ix)
                 for (int tx = xr[ix][0] / kMarkTileW; tx <= xr[ix][1] / kMarkTileW; ++tx) {
                     const int t = ty * m.tiles_x + tx;
-                    if (*reinterpret_cast<volatile int*>(m.epoch + t) == epoch) continue;
-                    if (atomicExch(m.epoch + t, epoch) != epoch) m.list[atomicAdd(&ctl->active_count, 1)] = t;
+                    // stamp the tile and count this mover; the first mover of the tick lists the tile
+                    unsigned old = *reinterpret_cast<volatile unsigned*>(m.epoch + t);
+                    for (;;) {
+                        const bool current = (old >> 12) == epoch;
+                        const unsigned n = current ? min((old & kMarkCountMax) + 1u, kMarkCountMax) : 1u;
+                        const unsigned prev = atomicCAS(m.epoch + t, old, (epoch << 12) | n);
+                        if (prev == old) {
+                            if (!current) m.list[atomicAdd(&ctl->active_count, 1)] = t;
+                            break;
+                        }
+                        old = prev;
+                    }
                 }
         }
 }
@@ -278,7 +291,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             if (from >= 0) ev[2 * from] = code;
             if (to >= 0) ev[2 * to + 1] = code;
             p.moved_dir[i] = (int8_t)d;
-            if (marks.epoch) mark_tiles(g, marks, ctl, (int)(ctl->tick % 0x7FFFFFF0ll) + 1, c.x, c.y, ux, uy, slab.active != 0);
+            if (marks.epoch) mark_tiles(g, marks, ctl, ctl->epoch, c.x, c.y, ux, uy, slab.active != 0);
             if (slab.active) { // remember the event cells for next tick's clear
                 const int at = atomicAdd(&ctl->ev_written_count, 2);
                 if (at + 1 < slab.ev_capacity) {
