@@ -82,9 +82,9 @@ WORKLOADS = {
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
-# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch at config 2, from the committed
-# ncu --set full capture (profiles/r1_k5_ncu_full_c2.txt); not re-measured by the bench run
-K5_DRAM_TRAFFIC_C2 = 53.756416e6 + 3.926784e6
+# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch (scatter kernel + dense gather kernel) at config 2,
+# from the committed ncu --set full capture (profiles/r1b_k5_c2.metrics.txt); not re-measured by the bench run
+K5_DRAM_TRAFFIC_C2 = (52.962304e6 + 3.445504e6) + (0.061184e6 + 0.0)
 BYTES_PER_SU_TICK = 200.0     # B_su
 BYTES_PER_PED_TICK = 200.0    # B_ped
 
@@ -412,9 +412,9 @@ def main():
         "data": "synthetic (seeded scenario, seed 42)",
         "config": {"workload": w["label"], "ticks_per_step": TICKS_PER_STEP, "cells": C, "pedestrians": P,
                    "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
-                   "l2": "no flush: the tick re-touches a 134 MB working set (96 MB images + 32 MB static + occupancy "
-                         "+ events) against a 126 MB L2, so steady-state ticks see L2 reuse; roofline.traffic "
-                         "reports the DRAM bytes actually moved"},
+                   "l2": f"no flush: the tick re-touches its whole working set ({134 * C / 1e6:.0f} MB: images, static image, "
+                         "occupancy, events) against a 126 MB L2; k-5 only touches su within reach of a mover, so "
+                         "roofline.traffic (DRAM bytes actually moved, ncu) is far below the algorithmic bytes"},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "pedestrian-steps/s",
                 "h2d_bytes_per_step": (ca["h2d_bytes"] - cb["h2d_bytes"]) // e2e_steps,
@@ -423,7 +423,7 @@ def main():
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
-        "roofline": {"bound": "hbm", "kernel": "k5_writeback_kernel", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k-5 write-back (all k-5 kernels of a tick)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": K5_DRAM_TRAFFIC_C2 if args.workload == "c2" else None,
                      "peak_source": peak_src, "bytes_per_launch": BYTES_PER_SU_K5 * C,
