@@ -79,6 +79,9 @@ struct sfc_engine {
     TileMarks marks{};     // active-tile list of k-5 (epoch stamps + list) as the kernels see it; epoch == nullptr: off
     TileMarks marks_alloc{}; // ... the allocation (the list is only switched on for sparse crowds, see sfc_upload)
     int k5_active_list = -1; // SFC_K5_ACTIVE_LIST: 0 never, 1 always, -1 by crowd density
+    WalkLists walk{};        // merged contributor lists of the list-walk kernel (meta == nullptr: not available)
+    int k5_listwalk = 1;     // dense tiles: list-walk kernel (SFC_K5_DENSE=gather: the event-walk gather)
+    int k5_listwalk_only = 0; // SFC_K5_PATH=listwalk: the list-walk kernel alone
     int sm_count = 148;
     Stager stager;
     bool uploaded = false;
@@ -385,6 +388,9 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.scatter_ctas = e->k5_scatter_ctas;
     l.marks = e->marks;
     l.window_path = e->k5_window;
+    l.walk = e->walk;
+    l.listwalk = e->k5_listwalk;
+    l.listwalk_only = e->k5_listwalk_only;
     return l;
 }
 
@@ -475,7 +481,11 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
-    if (const char* knob = std::getenv("SFC_K5_PATH")) e->k5_window_pref = std::string(knob) == "window";
+    if (const char* knob = std::getenv("SFC_K5_PATH")) {
+        e->k5_window_pref = std::string(knob) == "window";
+        e->k5_listwalk_only = std::string(knob) == "listwalk";
+    }
+    if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
@@ -513,6 +523,31 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         }
     }
     if (rc != SFC_OK) return bail(rc);
+    {   // merged contributor lists for the list-walk kernel, when the three kinds share them
+        WalkListsHost h;
+        if (build_walk_lists(*tables, &h) && h.n > 0) {
+            uint32_t *meta = nullptr, *masks = nullptr;
+            double* mag = nullptr;
+            bool ok = dev_alloc(&meta, h.n) == cudaSuccess;
+            if (ok) e->table_allocs.push_back(meta);
+            ok = ok && dev_alloc(&masks, h.n) == cudaSuccess;
+            if (ok) e->table_allocs.push_back(masks);
+            ok = ok && dev_alloc(&mag, (long long)h.n * kKinds) == cudaSuccess;
+            if (ok) e->table_allocs.push_back(mag);
+            ok = ok && cudaMemcpy(meta, h.meta.data(), sizeof(uint32_t) * h.meta.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+                 cudaMemcpy(masks, h.masks.data(), sizeof(uint32_t) * h.masks.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+                 cudaMemcpy(mag, h.mag.data(), sizeof(double) * h.mag.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+            if (!ok) return bail(fail(e, SFC_E_CUDA, "cudaMalloc / cudaMemcpy (contributor lists)"));
+            e->walk.meta = meta;
+            e->walk.masks = masks;
+            e->walk.mag = mag;
+            e->walk.n = h.n;
+            e->walk.hw = h.hw;
+            e->walk.hh = h.hh;
+            std::memcpy(e->walk.start, h.start, sizeof h.start);
+            std::memcpy(e->walk.sect_of, h.sect_of, sizeof h.sect_of);
+        }
+    }
 
     auto cu = [&](cudaError_t c, const char* what) {
         if (c != cudaSuccess && rc == SFC_OK) rc = cuda_fail(e, c, what);
@@ -584,6 +619,10 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(cudaMemset(e->dyn, 0, sizeof(float) * (size_t)e->cells * kKinds * kSects), "cudaMemset");
     cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
     cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
+    cu(prepare_k5_listwalk(cfg->chunk_k, e->walk, e->sm_count), "cudaFuncSetAttribute(k5 list walk)");
+    if (e->k5_tile_rows != kMarkTileH) e->k5_listwalk = e->k5_listwalk_only = 0; // (its tiles are 32 x 8)
+    if (e->k5_listwalk_only && !k5_listwalk_supported(e->walk)) e->k5_listwalk_only = 0;
+    if (e->k5_listwalk_only) e->k5_launches = 1;
     if (e->k5_window_ok)
         cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
@@ -720,7 +759,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         if (use != (e->marks.epoch != nullptr) || window != e->k5_window) {
             e->marks = use ? m : TileMarks{};
             e->k5_window = window;
-            e->k5_launches = window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max);
+            e->k5_launches = e->k5_listwalk_only ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
             e->graph_valid = false;
         }
         // the tick counter may restart: forget every epoch stamp

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "socfield_cuda.h"
 
 namespace sfc {
@@ -191,6 +193,25 @@ __host__ __device__ __forceinline__ int tile_edge_count(const TileMarks& m) {
     return (m.edge_lo + (m.tiles_y - m.edge_hi)) * m.tiles_x;
 }
 
+// Contributor lists for the list-walk formulation of k-5 (sfc_k5_listwalk.cu): the offsets of the
+// support grouped by the sect they feed (kind 0's sect; sect_of maps a group to kind k's sect),
+// each group in list order (rank 0, 1, 2, ...), shared by the three kinds.
+struct WalkLists {
+    const uint32_t* meta;  // [n] (dx + 128) | (dy + 128) << 8, centre offset = mover - target
+    const uint32_t* masks; // [n] orientation mask of kind k in byte k
+    const double* mag;     // [kind][n]
+    int n, hw, hh;
+    int start[kSects + 1]; // group g = entries [start[g], start[g + 1])
+    int sect_of[kKinds][kSects];
+};
+struct WalkListsHost {
+    std::vector<uint32_t> meta, masks;
+    std::vector<double> mag;
+    int n = 0, hw = 0, hh = 0;
+    int start[kSects + 1] = {};
+    int sect_of[kKinds][kSects] = {};
+};
+
 // ---- launchers (defined in the .cu files) --------------------------------------------------
 struct K5Launch {
     GridDev g;
@@ -206,7 +227,10 @@ struct K5Launch {
     int tile_rows;       // k-5: 8 (default) or 4 rows per tile on the two-kernel path
     int scatter_ctas;    // k-5: grid of the persistent scatter kernel
     TileMarks marks;     // k-5: active-tile list written by k-4 (epoch == nullptr: process every tile)
-    int window_path;     // k-5: 1 = window kernel + dense gather (default), 0 = legacy scatter + gather
+    int window_path;     // k-5: 1 = window kernel for sparse tiles, 0 = scatter kernel
+    WalkLists walk;      // k-5: merged contributor lists (meta == nullptr: the kinds do not share them)
+    int listwalk;        // k-5: dense tiles go to the list-walk kernel (1) or the event-walk gather (0)
+    int listwalk_only;   // k-5: the list-walk kernel is the only k-5 kernel (every / every active tile)
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
@@ -260,6 +284,11 @@ cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t);
 bool k5_window_supported(const TablesDev& t);
 cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count);
 cudaError_t launch_k5_window(cudaStream_t s, const K5Launch& a);
+// list-walk formulation of k-5 (sfc_k5_listwalk.cu)
+bool build_walk_lists(const sfc_tables& t, WalkListsHost* out);
+bool k5_listwalk_supported(const WalkLists& w);
+cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count);
+cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& a, bool from_dense_list);
 cudaError_t prepare_rebuild(const TablesDev& t);
 
 } // namespace sfc

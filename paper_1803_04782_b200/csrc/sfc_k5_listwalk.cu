@@ -1,0 +1,390 @@
+// sfc_k5_listwalk.cu — k-5 write-back for dense crowds on small fields: the reference's own
+// formulation (engine.cpp:428-472), one su per lane.
+//
+// For every (su, kind, sect) address the reference walks that sect's contributor list in order,
+// term idx = 2j (left) / 2j + 1 (arrived) for the j-th contributor, partial = idx mod K, partials
+// folded in slot order (accumulator.hpp:36-46).  The slot depends on the LIST POSITION only, so a
+// walk unrolled by K / 2 positions has compile-time slots: the K partials of an address live in
+// registers, every lane of a warp runs the same instruction stream (one su each, 32 su of a tile
+// row), and the result is the reference's bit for bit with no replay, no atomics, no sorting —
+// whatever the number of movers.  Adding +-0.0 never changes a partial, so positions where no lane
+// of the warp sees an event are skipped with one ballot.
+//
+// The three kinds share the walk when they have the same support and list ranks (they do whenever
+// they share a field geometry: a repulsive kind's sect is the attractive kind's opposite, so the
+// sect GROUPS of offsets coincide): one event-code load per position serves six gated terms.
+//
+// A CTA takes a 32 x 8 su tile — from the dense-tile list the scatter / window kernel filled, or
+// every (active) tile when this is the only k-5 kernel — stages tile + field halo of the event map
+// in shared memory (coalesced, loads batched), and warp w walks row w.  Cost per su is 6F gated
+// adds at most, independent of the crowd: the dense-crowd path for fields up to 15 x 15.
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "sfc_internal.cuh"
+
+namespace sfc {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kListSmemMax = 256; // merged list entries kept in shared memory (15 x 15 fields: 224)
+
+struct LwArgs {
+    GridDev g;
+    WalkLists w;
+    float* dyn;
+    const uint8_t* ev;
+    Ctl* ctl;
+    TileMarks marks;       // every-tile mode: active-tile list (epoch == nullptr: all tiles)
+    const int* dense_list; // dense-list mode: tiles handed over by the scatter / window kernel
+    int from_dense_list;
+    int advance_tick;
+    int tiles_x, n_tiles;
+    int rwf, rwp, rh;      // region columns, code row pitch (u16), region rows of a full tile
+    int list_smem;
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!a.from_dense_list && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
+    if (a.ctl->error_code != 0) return;
+
+    const int n = a.w.n;
+    float* const tot = reinterpret_cast<float*>(smem_raw);                          // [kind * 8 + sect][kThreads]
+    double* const s_mag = reinterpret_cast<double*>(tot + kKinds * kSects * kThreads); // [kind][n]
+    uint32_t* const s_meta = reinterpret_cast<uint32_t*>(s_mag + (a.list_smem ? kKinds * n : 0));
+    uint32_t* const s_masks = s_meta + (a.list_smem ? n : 0);
+    long long* const rowoff = reinterpret_cast<long long*>(s_masks + (a.list_smem ? ((n + 1) & ~1) : 0)); // [rh]
+    uint16_t* const codes = reinterpret_cast<uint16_t*>(rowoff + a.rh);              // [rh][rwp]
+    if (a.list_smem) {
+        for (int i = tid; i < n; i += kThreads) {
+            s_meta[i] = a.w.meta[i];
+            s_masks[i] = a.w.masks[i];
+            for (int k = 0; k < kKinds; ++k) s_mag[k * n + i] = a.w.mag[k * n + i];
+        }
+    }
+    const uint32_t* const meta = a.list_smem ? s_meta : a.w.meta;
+    const uint32_t* const masks = a.list_smem ? s_masks : a.w.masks;
+    const double* const mag = a.list_smem ? s_mag : a.w.mag;
+
+    const GridDev g = a.g;
+    const int HW = a.w.hw, HH = a.w.hh;
+    const int RWF = a.rwf, RWP = a.rwp;
+    const bool narrow = RWF <= g.W;
+    const uint16_t* const ev16 = reinterpret_cast<const uint16_t*>(a.ev);
+    const unsigned inv_rwf = 0xFFFFFFFFu / (unsigned)RWF + 1u;
+    int n_items, n_edge = 0;
+    if (a.from_dense_list) {
+        n_items = a.ctl->dense_count;
+    } else if (a.marks.epoch != nullptr) {
+        n_edge = tile_edge_count(a.marks);
+        n_items = n_edge + a.ctl->active_count;
+    } else {
+        n_items = a.n_tiles;
+    }
+
+    for (int item = (int)blockIdx.x; item < n_items; item += (int)gridDim.x) {
+        int tile;
+        if (a.from_dense_list) {
+            tile = a.dense_list[item];
+        } else if (a.marks.epoch == nullptr) {
+            tile = item;
+        } else if (item < n_edge) { // slab mode: tiles whose region reaches the halo rows
+            const int r = item / a.tiles_x;
+            const int ty = r < a.marks.edge_lo ? r : a.marks.edge_hi + (r - a.marks.edge_lo);
+            tile = ty * a.tiles_x + (item - r * a.tiles_x);
+        } else {
+            tile = a.marks.list[item - n_edge];
+        }
+        const int tile_y = tile / a.tiles_x, tile_x = tile - tile_y * a.tiles_x;
+        const int x0 = tile_x * kMarkTileW;
+        const int y0 = g.row0 + tile_y * kMarkTileH;
+        const int nx = min(kMarkTileW, g.W - x0);
+        const int ny = min(kMarkTileH, g.row0 + g.rows - y0);
+        const int RH = ny + 2 * HH;
+        const int xs = x0 - HW, ys = y0 - HH;
+
+        // ---- stage (CTA) ---------------------------------------------------------------------
+        __syncthreads(); // the previous tile is done with codes / rowoff (and the lists are loaded)
+        for (int ry = tid; ry < RH; ry += kThreads) rowoff[ry] = cell_index(g, 0, ys + ry); // -1: no such row / not resident
+        __syncthreads();
+        bool any = false;
+        {
+            const int n_cells = RWF * RH;
+            for (int i0 = 0; i0 < n_cells; i0 += 4 * kThreads) {
+                uint32_t got[4];
+                int at[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { // the loads of the chunk fly together
+                    const int i = i0 + q * kThreads + tid;
+                    got[q] = 0u;
+                    at[q] = -1;
+                    if (i < n_cells) {
+                        const int ry = (int)__umulhi((unsigned)i, inv_rwf); // i / RWF
+                        const int c = i - ry * RWF;
+                        at[q] = ry * RWP + c;
+                        int x = xs + c;
+                        if (g.closed) {
+                            if (x < 0 || x >= g.W) x = -1;
+                        } else if (narrow) {
+                            x += x < 0 ? g.W : (x >= g.W ? -g.W : 0);
+                        } else {
+                            x = emod(x, g.W);
+                        }
+                        const long long ro = rowoff[ry];
+                        if (ro >= 0 && x >= 0) got[q] = __ldg(ev16 + ro + x);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (at[q] >= 0) {
+                        codes[at[q]] = (uint16_t)got[q];
+                        any |= got[q] != 0u;
+                    }
+            }
+        }
+        if (__syncthreads_or(any ? 1 : 0) == 0) continue; // nobody moved within reach of this tile
+
+        // ---- walk (lane: one su of tile row `warp`) -------------------------------------------
+        const bool valid = lane < nx && warp < ny;
+        const uint16_t* const centre = codes + (warp + HH) * RWP + lane + HW; // my su in the staged region
+        bool touched = false;
+#pragma unroll 1
+        for (int grp = 0; grp < kSects; ++grp) {
+            double p[kKinds][K];
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k)
+#pragma unroll
+                for (int q = 0; q < K; ++q) p[k][q] = 0.0;
+            const int j_end = a.w.start[grp + 1];
+            for (int j0 = a.w.start[grp]; j0 < j_end; j0 += K / 2) {
+#pragma unroll
+                for (int u = 0; u < K / 2; ++u) { // list position j0 + u: term idx 2u (left), 2u + 1 (arrived) mod K
+                    const int j = j0 + u;
+                    if (j >= j_end) break; // uniform
+                    const uint32_t m = meta[j];
+                    const int dx = (int)(m & 0xFFu) - 128, dy = (int)((m >> 8) & 0xFFu) - 128; // centre offset = mover - target
+                    const uint32_t code = valid ? centre[dy * RWP + dx] : 0u;
+                    if (__ballot_sync(0xFFFFFFFFu, code != 0u) == 0u) continue; // zero terms never change a partial
+                    const uint32_t mk = masks[j];
+                    const uint32_t fb = code & 0xFFu, tb = code >> 8;
+                    const bool hf = fb & 0x80u, ht = tb & 0x80u;
+#pragma unroll
+                    for (int k = 0; k < kKinds; ++k) {
+                        const uint32_t mask = (mk >> (8 * k)) & 0xFFu;
+                        // orientation of the mover's field of this kind; kind 2 is non-directional (orientation 0)
+                        const uint32_t of = k == 0 ? (fb & 7u) : (k == 1 ? ((fb >> 3) & 7u) : 0u);
+                        const uint32_t ot = k == 0 ? (tb & 7u) : (k == 1 ? ((tb >> 3) & 7u) : 0u);
+                        const bool from = hf && ((mask >> of) & 1u), to = ht && ((mask >> ot) & 1u);
+                        const double mg = mag[k * n + j];
+                        if (from) p[k][2 * u] = __dadd_rn(p[k][2 * u], -mg);
+                        if (to) p[k][2 * u + 1] = __dadd_rn(p[k][2 * u + 1], mg);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                double total = 0.0; // StepCache::total, slot order
+#pragma unroll
+                for (int q = 0; q < K; ++q) total = __dadd_rn(total, p[k][q]);
+                const float add = __double2float_rn(total);
+                tot[(k * kSects + a.w.sect_of[k][grp]) * kThreads + tid] = add;
+                touched |= add != 0.0f;
+            }
+        }
+
+        // ---- apply: image += (float)total, one 32-byte sector per touched (su, kind) ------------
+        if (valid && touched) {
+            float4* const rec = reinterpret_cast<float4*>(a.dyn + (rowoff[warp + HH] + x0 + lane) * (kKinds * kSects));
+#pragma unroll
+            for (int k = 0; k < kKinds; ++k) {
+                float t[8];
+                bool nz = false;
+#pragma unroll
+                for (int s = 0; s < kSects; ++s) {
+                    t[s] = tot[(k * kSects + s) * kThreads + tid];
+                    nz |= t[s] != 0.0f;
+                }
+                if (!nz) continue;
+                const float4 v0 = rec[2 * k], v1 = rec[2 * k + 1];
+                rec[2 * k] = make_float4(__fadd_rn(v0.x, t[0]), __fadd_rn(v0.y, t[1]), __fadd_rn(v0.z, t[2]), __fadd_rn(v0.w, t[3]));
+                rec[2 * k + 1] = make_float4(__fadd_rn(v1.x, t[4]), __fadd_rn(v1.y, t[5]), __fadd_rn(v1.z, t[6]), __fadd_rn(v1.w, t[7]));
+            }
+        }
+    }
+}
+
+struct LwShape {
+    size_t smem;
+    int rwf, rwp, rh, list_smem;
+};
+
+LwShape lw_shape(const WalkLists& w) {
+    LwShape s;
+    s.rwf = kMarkTileW + 2 * w.hw;
+    s.rwp = (s.rwf + 1) & ~1;
+    s.rh = kMarkTileH + 2 * w.hh;
+    s.list_smem = w.n <= kListSmemMax;
+    size_t b = sizeof(float) * kKinds * kSects * kThreads;
+    if (s.list_smem) b += sizeof(double) * kKinds * w.n + sizeof(uint32_t) * (w.n + ((w.n + 1) & ~1));
+    b = (b + 7) & ~(size_t)7;
+    b += sizeof(long long) * s.rh;
+    b += sizeof(uint16_t) * (size_t)s.rwp * s.rh;
+    s.smem = (b + 15) & ~(size_t)15;
+    return s;
+}
+
+struct LwPrepared {
+    size_t granted = 0;
+    int ctas = 0;
+};
+LwPrepared g_prepared[4];
+
+template <int K>
+cudaError_t prepare_one(const WalkLists& w, int sm_count, LwPrepared& st) {
+    const LwShape sh = lw_shape(w);
+    if (sh.smem > st.granted) {
+        const cudaError_t e = cudaFuncSetAttribute(k5_listwalk_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+        if (e != cudaSuccess) return e;
+        st.granted = sh.smem;
+    }
+    int per_sm = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_listwalk_kernel<K>, kThreads, sh.smem);
+    if (e != cudaSuccess) return e;
+    st.ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+    return cudaSuccess;
+}
+
+template <int K>
+cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_list, const LwPrepared& st) {
+    const LwShape sh = lw_shape(l.walk);
+    LwArgs a;
+    a.g = l.g;
+    a.w = l.walk;
+    a.dyn = l.dyn;
+    a.ev = l.ev;
+    a.ctl = l.ctl;
+    a.marks = from_dense_list ? TileMarks{} : l.marks;
+    a.dense_list = l.dense_list;
+    a.from_dense_list = from_dense_list ? 1 : 0;
+    a.advance_tick = l.advance_tick;
+    a.tiles_x = (l.g.W + kMarkTileW - 1) / kMarkTileW;
+    a.n_tiles = a.tiles_x * ((l.g.rows + kMarkTileH - 1) / kMarkTileH);
+    a.rwf = sh.rwf;
+    a.rwp = sh.rwp;
+    a.rh = sh.rh;
+    a.list_smem = sh.list_smem;
+    long long blocks = a.n_tiles;
+    if (blocks > st.ctas) blocks = st.ctas;
+    if (blocks < 1) blocks = 1;
+    k5_listwalk_kernel<K><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+int k_index(int chunk_k) { return chunk_k == 2 ? 0 : (chunk_k == 4 ? 1 : (chunk_k == 8 ? 2 : 3)); }
+
+} // namespace
+
+// Builds the merged per-sect-group contributor lists from the three kind tables (host copies).
+// Returns false — the list walk is then not used — when the kinds do not share support and ranks.
+bool build_walk_lists(const sfc_tables& t, WalkListsHost* out) {
+    const int fw = t.kind[0].width, fh = t.kind[0].height;
+    for (int k = 1; k < kKinds; ++k)
+        if (t.kind[k].width != fw || t.kind[k].height != fh) return false;
+    if (fw > 255 || fh > 255) return false;
+    const int hw = (fw - 1) / 2, hh = (fh - 1) / 2;
+    struct Entry {
+        int sect0, rank, dx, dy, at;
+    };
+    std::vector<Entry> entries;
+    for (int dy = -hh; dy <= hh; ++dy)
+        for (int dx = -hw; dx <= hw; ++dx) {
+            const int at = (dy + hh) * fw + dx + hw;
+            const uint32_t i0 = t.kind[0].info[at];
+            const bool in0 = ((i0 >> 3) & 0xFFu) != 0u;
+            for (int k = 1; k < kKinds; ++k) {
+                const uint32_t ik = t.kind[k].info[at];
+                if ((((ik >> 3) & 0xFFu) != 0u) != in0) return false;  // different support
+                if (in0 && (ik >> 11) != (i0 >> 11)) return false;      // different list rank
+            }
+            if (in0) entries.push_back(Entry{(int)(i0 & 7u), (int)(i0 >> 11), dx, dy, at});
+        }
+    std::sort(entries.begin(), entries.end(),
+              [](const Entry& x, const Entry& y) { return x.sect0 != y.sect0 ? x.sect0 < y.sect0 : x.rank < y.rank; });
+    WalkListsHost& w = *out;
+    w.n = (int)entries.size();
+    w.hw = hw;
+    w.hh = hh;
+    w.meta.assign((size_t)w.n, 0u);
+    w.masks.assign((size_t)w.n, 0u);
+    w.mag.assign((size_t)w.n * kKinds, 0.0);
+    for (int s = 0; s <= kSects; ++s) w.start[s] = 0;
+    for (int k = 0; k < kKinds; ++k)
+        for (int s = 0; s < kSects; ++s) w.sect_of[k][s] = -1;
+    for (int i = 0; i < w.n; ++i) {
+        const Entry& e = entries[(size_t)i];
+        if (i > 0 && entries[(size_t)i - 1].sect0 == e.sect0 && entries[(size_t)i - 1].rank + 1 != e.rank) return false;
+        if ((i == 0 || entries[(size_t)i - 1].sect0 != e.sect0) && e.rank != 0) return false; // ranks must be 0, 1, 2, ...
+        w.start[e.sect0 + 1] += 1;
+        w.meta[(size_t)i] = (uint32_t)(e.dx + 128) | ((uint32_t)(e.dy + 128) << 8);
+        for (int k = 0; k < kKinds; ++k) {
+            const uint32_t ik = t.kind[k].info[e.at];
+            w.masks[(size_t)i] |= ((ik >> 3) & 0xFFu) << (8 * k);
+            w.mag[(size_t)k * w.n + i] = t.kind[k].magnitude[e.at];
+            int& mapped = w.sect_of[k][e.sect0];
+            if (mapped < 0) mapped = (int)(ik & 7u);
+            if (mapped != (int)(ik & 7u)) return false; // a group of kind 0 must be one group of kind k
+        }
+    }
+    for (int s = 0; s < kSects; ++s) w.start[s + 1] += w.start[s];
+    for (int k = 0; k < kKinds; ++k) { // the map must be a permutation (empty groups take the unused sects)
+        bool used[kSects] = {};
+        for (int s = 0; s < kSects; ++s)
+            if (w.sect_of[k][s] >= 0) {
+                if (used[w.sect_of[k][s]]) return false;
+                used[w.sect_of[k][s]] = true;
+            }
+        for (int s = 0; s < kSects; ++s)
+            if (w.sect_of[k][s] < 0)
+                for (int q = 0; q < kSects; ++q)
+                    if (!used[q]) {
+                        w.sect_of[k][s] = q;
+                        used[q] = true;
+                        break;
+                    }
+    }
+    return true;
+}
+
+// Fields up to 15 x 15 (the per-su cost grows with the field area whatever the crowd).
+bool k5_listwalk_supported(const WalkLists& w) { return w.meta != nullptr && w.n > 0 && w.n <= kListSmemMax; }
+
+cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count) {
+    if (!k5_listwalk_supported(w)) return cudaSuccess;
+    LwPrepared& st = g_prepared[k_index(chunk_k)];
+    switch (chunk_k) {
+        case 2: return prepare_one<2>(w, sm_count, st);
+        case 4: return prepare_one<4>(w, sm_count, st);
+        case 8: return prepare_one<8>(w, sm_count, st);
+        case 16: return prepare_one<16>(w, sm_count, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& l, bool from_dense_list) {
+    const LwPrepared& st = g_prepared[k_index(l.chunk_k)];
+    switch (l.chunk_k) {
+        case 2: return launch_one<2>(s, l, from_dense_list, st);
+        case 4: return launch_one<4>(s, l, from_dense_list, st);
+        case 8: return launch_one<8>(s, l, from_dense_list, st);
+        case 16: return launch_one<16>(s, l, from_dense_list, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+} // namespace sfc

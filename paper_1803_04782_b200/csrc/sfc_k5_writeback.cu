@@ -756,11 +756,13 @@ cudaError_t prepare_k(const TablesDev& t) {
 
 template <int K, int SG>
 cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
+    const bool walk = l.listwalk && k5_listwalk_supported(l.walk); // dense 32 x 8 tiles: list walk instead of event walk
+    if (l.listwalk_only && walk) return launch_k5_listwalk(s, l, false);
     if (l.window_path && k5_window_supported(l.t) && l.dense_list != nullptr) {
-        // window kernel over the active tiles; it hands dense tiles (32 x 8) to the gather kernel
+        // window kernel over the active tiles; it hands dense tiles (32 x 8) to the dense kernel
         const cudaError_t e = launch_k5_window(s, l);
         if (e != cudaSuccess) return e;
-        return launch_one<K, SG, 2, 128, kModeDense>(s, l);
+        return walk ? launch_k5_listwalk(s, l, true) : launch_one<K, SG, 2, 128, kModeDense>(s, l);
     }
     // large fields: 32 x 16 tiles (the field halo is staged once per 512 su), gather only
     if (!two_kernel_path(l.t)) return launch_one<K, SG, 4, 128, kModeAll>(s, l);
@@ -772,7 +774,7 @@ cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
     }
     const cudaError_t e = launch_one<K, SG, 2, 256, kModeScatter>(s, l);
     if (e != cudaSuccess) return e;
-    return launch_one<K, SG, 2, 128, kModeDense>(s, l);
+    return walk ? launch_k5_listwalk(s, l, true) : launch_one<K, SG, 2, 128, kModeDense>(s, l);
 }
 
 } // namespace
