@@ -47,7 +47,13 @@ struct LwArgs {
     int list_smem;
 };
 
-template <int K>
+// p += t when flag != 0, as ONE predicated DADD (the compiler's if-conversion would emit an
+// unconditional add followed by two selects per 64-bit partial).
+__device__ __forceinline__ void add_if(double& p, double t, uint32_t flag) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}" : "+d"(p) : "d"(t), "r"(flag));
+}
+
+template <int K, bool LIST_SMEM>
 __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -57,20 +63,20 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
     const int n = a.w.n;
     float* const tot = reinterpret_cast<float*>(smem_raw);                          // [kind * 8 + sect][kThreads]
     double* const s_mag = reinterpret_cast<double*>(tot + kKinds * kSects * kThreads); // [kind][n]
-    uint32_t* const s_meta = reinterpret_cast<uint32_t*>(s_mag + (a.list_smem ? kKinds * n : 0));
-    uint32_t* const s_masks = s_meta + (a.list_smem ? n : 0);
-    long long* const rowoff = reinterpret_cast<long long*>(s_masks + (a.list_smem ? ((n + 1) & ~1) : 0)); // [rh]
-    uint16_t* const codes = reinterpret_cast<uint16_t*>(rowoff + a.rh);              // [rh][rwp]
-    if (a.list_smem) {
+    uint32_t* const s_meta = reinterpret_cast<uint32_t*>(s_mag + (LIST_SMEM ? kKinds * n : 0));
+    uint32_t* const s_masks = s_meta + (LIST_SMEM ? n : 0);
+    long long* const rowoff = reinterpret_cast<long long*>(s_masks + (LIST_SMEM ? ((n + 1) & ~1) : 0)); // [rh]
+    // per region cell: one-hot orientation selectors of the event that left it (.x) / arrived at it (.y),
+    // per kind in the byte lanes of the mask words (kind 2 is non-directional: orientation 0); 0 = no event
+    uint2* const sel = reinterpret_cast<uint2*>(rowoff + a.rh);                      // [rh][rwp]
+    if (LIST_SMEM) {
         for (int i = tid; i < n; i += kThreads) {
-            s_meta[i] = a.w.meta[i];
+            const uint32_t m = a.w.meta[i];
+            s_meta[i] = (uint32_t)(((int)((m >> 8) & 0xFFu) - 128) * a.rwp + ((int)(m & 0xFFu) - 128)); // cell offset dy * pitch + dx
             s_masks[i] = a.w.masks[i];
             for (int k = 0; k < kKinds; ++k) s_mag[k * n + i] = a.w.mag[k * n + i];
         }
     }
-    const uint32_t* const meta = a.list_smem ? s_meta : a.w.meta;
-    const uint32_t* const masks = a.list_smem ? s_masks : a.w.masks;
-    const double* const mag = a.list_smem ? s_mag : a.w.mag;
 
     const GridDev g = a.g;
     const int HW = a.w.hw, HH = a.w.hh;
@@ -143,7 +149,9 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (at[q] >= 0) {
-                        codes[at[q]] = (uint16_t)got[q];
+                        const uint32_t fb = got[q] & 0xFFu, tb = got[q] >> 8;
+                        sel[at[q]] = make_uint2((fb & 0x80u) ? ((1u << (fb & 7u)) | (256u << ((fb >> 3) & 7u)) | 0x10000u) : 0u,
+                                                (tb & 0x80u) ? ((1u << (tb & 7u)) | (256u << ((tb >> 3) & 7u)) | 0x10000u) : 0u);
                         any |= got[q] != 0u;
                     }
             }
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
 
         // ---- walk (lane: one su of tile row `warp`) -------------------------------------------
         const bool valid = lane < nx && warp < ny;
-        const uint16_t* const centre = codes + (warp + HH) * RWP + lane + HW; // my su in the staged region
+        const uint2* const centre = sel + (warp + HH) * RWP + lane + HW; // my su in the staged region
         bool touched = false;
 #pragma unroll 1
         for (int grp = 0; grp < kSects; ++grp) {
@@ -167,23 +175,22 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
                 for (int u = 0; u < K / 2; ++u) { // list position j0 + u: term idx 2u (left), 2u + 1 (arrived) mod K
                     const int j = j0 + u;
                     if (j >= j_end) break; // uniform
-                    const uint32_t m = meta[j];
-                    const int dx = (int)(m & 0xFFu) - 128, dy = (int)((m >> 8) & 0xFFu) - 128; // centre offset = mover - target
-                    const uint32_t code = valid ? centre[dy * RWP + dx] : 0u;
-                    if (__ballot_sync(0xFFFFFFFFu, code != 0u) == 0u) continue; // zero terms never change a partial
-                    const uint32_t mk = masks[j];
-                    const uint32_t fb = code & 0xFFu, tb = code >> 8;
-                    const bool hf = fb & 0x80u, ht = tb & 0x80u;
+                    int off; // cell offset of the contributor: centre offset = mover - target
+                    if (LIST_SMEM) {
+                        off = (int)s_meta[j];
+                    } else {
+                        const uint32_t m = __ldg(a.w.meta + j);
+                        off = ((int)((m >> 8) & 0xFFu) - 128) * RWP + ((int)(m & 0xFFu) - 128);
+                    }
+                    const uint2 c = valid ? centre[off] : make_uint2(0u, 0u);
+                    if (__ballot_sync(0xFFFFFFFFu, (c.x | c.y) != 0u) == 0u) continue; // zero terms never change a partial
+                    const uint32_t mk = LIST_SMEM ? s_masks[j] : __ldg(a.w.masks + j); // orientation mask of kind k in byte k
+                    const uint32_t fbits = mk & c.x, tbits = mk & c.y; // gating the six terms is two ANDs
 #pragma unroll
                     for (int k = 0; k < kKinds; ++k) {
-                        const uint32_t mask = (mk >> (8 * k)) & 0xFFu;
-                        // orientation of the mover's field of this kind; kind 2 is non-directional (orientation 0)
-                        const uint32_t of = k == 0 ? (fb & 7u) : (k == 1 ? ((fb >> 3) & 7u) : 0u);
-                        const uint32_t ot = k == 0 ? (tb & 7u) : (k == 1 ? ((tb >> 3) & 7u) : 0u);
-                        const bool from = hf && ((mask >> of) & 1u), to = ht && ((mask >> ot) & 1u);
-                        const double mg = mag[k * n + j];
-                        if (from) p[k][2 * u] = __dadd_rn(p[k][2 * u], -mg);
-                        if (to) p[k][2 * u + 1] = __dadd_rn(p[k][2 * u + 1], mg);
+                        const double mg = LIST_SMEM ? s_mag[k * n + j] : __ldg(a.w.mag + k * n + j);
+                        add_if(p[k][2 * u], -mg, fbits & (0xFFu << (8 * k)));
+                        add_if(p[k][2 * u + 1], mg, tbits & (0xFFu << (8 * k)));
                     }
                 }
             }
@@ -234,7 +241,7 @@ LwShape lw_shape(const WalkLists& w) {
     if (s.list_smem) b += sizeof(double) * kKinds * w.n + sizeof(uint32_t) * (w.n + ((w.n + 1) & ~1));
     b = (b + 7) & ~(size_t)7;
     b += sizeof(long long) * s.rh;
-    b += sizeof(uint16_t) * (size_t)s.rwp * s.rh;
+    b += sizeof(uint2) * (size_t)s.rwp * s.rh;
     s.smem = (b + 15) & ~(size_t)15;
     return s;
 }
@@ -249,12 +256,12 @@ template <int K>
 cudaError_t prepare_one(const WalkLists& w, int sm_count, LwPrepared& st) {
     const LwShape sh = lw_shape(w);
     if (sh.smem > st.granted) {
-        const cudaError_t e = cudaFuncSetAttribute(k5_listwalk_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+        const cudaError_t e = cudaFuncSetAttribute(k5_listwalk_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
         if (e != cudaSuccess) return e;
         st.granted = sh.smem;
     }
     int per_sm = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_listwalk_kernel<K>, kThreads, sh.smem);
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_listwalk_kernel<K, true>, kThreads, sh.smem);
     if (e != cudaSuccess) return e;
     st.ctas = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
@@ -282,7 +289,7 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_l
     long long blocks = a.n_tiles;
     if (blocks > st.ctas) blocks = st.ctas;
     if (blocks < 1) blocks = 1;
-    k5_listwalk_kernel<K><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a);
+    k5_listwalk_kernel<K, true><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a); // (supported lists always fit: kListSmemMax)
     return cudaGetLastError();
 }
 
