@@ -81,7 +81,8 @@ struct sfc_engine {
     int k5_active_list = -1; // SFC_K5_ACTIVE_LIST: 0 never, 1 always, -1 by crowd density
     WalkLists walk{};        // merged contributor lists of the list-walk kernel (meta == nullptr: not available)
     int k5_listwalk = 1;     // dense tiles: list-walk kernel (SFC_K5_DENSE=gather: the event-walk gather)
-    int k5_listwalk_only = 0; // SFC_K5_PATH=listwalk: the list-walk kernel alone
+    int k5_listwalk_only = 0; // the list-walk kernel alone (chosen in sfc_upload, or SFC_K5_PATH=listwalk)
+    int k5_path_pref = -1;    // SFC_K5_PATH: 0 scatter, 1 window, 2 listwalk, -1 by crowd and field (sfc_upload)
     int sm_count = 148;
     Stager stager;
     bool uploaded = false;
@@ -482,8 +483,9 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
-        e->k5_window_pref = std::string(knob) == "window";
-        e->k5_listwalk_only = std::string(knob) == "listwalk";
+        const std::string path(knob);
+        e->k5_path_pref = path == "window" ? 1 : (path == "listwalk" ? 2 : 0);
+        e->k5_window_pref = path == "window";
     }
     if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
@@ -620,9 +622,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
     cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
     cu(prepare_k5_listwalk(cfg->chunk_k, e->walk, e->sm_count), "cudaFuncSetAttribute(k5 list walk)");
-    if (e->k5_tile_rows != kMarkTileH) e->k5_listwalk = e->k5_listwalk_only = 0; // (its tiles are 32 x 8)
-    if (e->k5_listwalk_only && !k5_listwalk_supported(e->walk)) e->k5_listwalk_only = 0;
-    if (e->k5_listwalk_only) e->k5_launches = 1;
+    if (e->k5_tile_rows != kMarkTileH || !k5_listwalk_supported(e->walk)) e->k5_listwalk = 0; // (its tiles are 32 x 8)
     if (e->k5_window_ok)
         cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
@@ -752,14 +752,19 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         const long long per_mover = (long long)((2 * m.hw + 1) / kMarkTileW + 2) * ((2 * m.hh + 1) / kMarkTileH + 2);
         const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
         const bool sparse = P * per_mover < 2 * n_tiles; // (expected share of active tiles below ~85 %)
-        // sparse crowds: the window kernel (its per-tile cost is the lower one when a tile holds an
-        // event or two); otherwise the scatter kernel, which puts a whole CTA on every tile
-        const int window = e->k5_window_ok && (e->k5_window_pref == 1 || (e->k5_window_pref < 0 && sparse));
+        // Which k-5 formulation (all bit-identical; measured in profiles/README.md):
+        //   sparse crowd                 -> window kernel over the active-tile list (dense tiles: list walk / gather)
+        //   else, fields up to 11 x 11   -> the list-walk kernel alone: per-su cost fixed by the field area, at or
+        //                                   below the scatter kernel's from corridor densities up, far below for crowds
+        //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
+        const int window = e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
+        const int walk_only = !window && e->k5_listwalk && (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
         const bool use = window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse);
-        if (use != (e->marks.epoch != nullptr) || window != e->k5_window) {
+        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only) {
             e->marks = use ? m : TileMarks{};
             e->k5_window = window;
-            e->k5_launches = e->k5_listwalk_only ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
+            e->k5_listwalk_only = walk_only;
+            e->k5_launches = walk_only ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
             e->graph_valid = false;
         }
         // the tick counter may restart: forget every epoch stamp

@@ -128,13 +128,16 @@ def test_against_compiled_reference(product_lib, ref_lib):
                 np.testing.assert_array_equal(bits(gpu.image(k)), bits(ref.image(k)))
 
 
-@pytest.mark.parametrize("knob", ["0", "100000"])
+@pytest.mark.parametrize("knob,dense", [("0", "gather"), ("100000", "gather"), ("3", "gather"), ("3", "listwalk")])
 @pytest.mark.parametrize("name", ["desk64", "k2", "k4", "k16", "field-5x9", "field-bigger-than-grid", "closed-four",
                                   "wide-ragged", "d0.1-eight-ped1", "d0.9-four-ped3"])
-def test_both_k5_formulations(product_lib, monkeypatch, name, knob):
-    """k-5 has two formulations chosen per tile by the number of movers in reach: an event-centric
-    scatter (sparse tiles) and a su-centric gather (dense tiles).  SFC_K5_EVENT_MAX forces every
-    tile through one or the other; both must be bit-identical to the oracle."""
+def test_both_k5_formulations(product_lib, monkeypatch, name, knob, dense):
+    """The scatter path of k-5 chooses per tile by the number of movers in reach: an event-centric
+    scatter (sparse tiles) or a dense kernel — the event-walk gather or the list walk.
+    SFC_K5_EVENT_MAX forces every tile through one or the other (0: the gather alone, 100000: the
+    scatter alone, 3: nearly every tile handed to the dense kernel); all bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_PATH", "scatter")
+    monkeypatch.setenv("SFC_K5_DENSE", dense)
     monkeypatch.setenv("SFC_K5_EVENT_MAX", knob)
     text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
     gpu = shim.Sim.from_scenario(product_lib, text)
@@ -144,7 +147,8 @@ def test_both_k5_formulations(product_lib, monkeypatch, name, knob):
         assert_state_equal(gpu, cpu, f"{name} knob {knob} tick {8 * (step + 1)}")
 
 
-@pytest.mark.parametrize("path,knob", [("window", None), ("window", "100000"), ("window", "2"), ("scatter-list", None)])
+@pytest.mark.parametrize("path,knob", [("window", None), ("window", "100000"), ("window", "2"), ("scatter-list", None),
+                                       ("listwalk", None), ("listwalk-list", None)])
 @pytest.mark.parametrize("name", ["desk64", "k2", "k16", "field-5x9", "field21", "field-bigger-than-grid", "closed-four",
                                   "closed-ped3", "ped5", "wide-ragged", "sparse-periodic", "sparse-closed", "sparse-field15",
                                   "d0.9-four-ped3"])
@@ -153,11 +157,10 @@ def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path,
     crowds also switch to the window kernel (one warp per 8 x 4 su block, event-major scatter, exact
     replay).  Forced here on crowds of every density: the window kernel with its default hand-off
     to the dense gather, with every tile kept (knob 100000) or nearly every tile handed off (2), and
-    the scatter kernel driven from the list.  All bit-identical to the oracle."""
-    if path == "window":
-        monkeypatch.setenv("SFC_K5_PATH", "window")
-    else:
-        monkeypatch.setenv("SFC_K5_PATH", "scatter")
+    the scatter kernel driven from the list, the list-walk kernel alone over every tile and over the
+    listed tiles.  All bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_PATH", path.split("-")[0])
+    if path.endswith("-list"):
         monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "1")
     if knob is not None:
         monkeypatch.setenv("SFC_K5_EVENT_MAX", knob)

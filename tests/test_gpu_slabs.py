@@ -40,13 +40,13 @@ def test_slabs_equal_undivided_grid(product_lib, monkeypatch, name, slabs):
 
 @pytest.mark.parametrize("name,slabs", [("desk64", 2), ("closed-four", 2), ("wide-ragged", 3), ("field21", 2),
                                         ("sparse-periodic", 3), ("sparse-closed", 2), ("sparse-field15", 2)])
-@pytest.mark.parametrize("path", ["window", "scatter-list"])
+@pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list"])
 def test_slabs_with_active_tile_list(product_lib, monkeypatch, name, slabs, path):
     """Slabs keep the tiles whose field region reaches into the halo rows permanently active (the
     neighbours' events arrive there as row copies, unseen by this slab's k-4) and list the rest."""
     monkeypatch.setenv("SFC_SLABS", str(slabs))
-    monkeypatch.setenv("SFC_K5_PATH", "window" if path == "window" else "scatter")
-    if path != "window":
+    monkeypatch.setenv("SFC_K5_PATH", path.split("-")[0])
+    if path.endswith("-list"):
         monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "1")
     text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
     gpu = shim.Sim.from_scenario(product_lib, text)
