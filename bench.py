@@ -82,9 +82,9 @@ WORKLOADS = {
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
-# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch (scatter kernel + dense gather kernel) at config 2,
-# from the committed ncu --set full capture (profiles/r1b_k5_c2.metrics.txt); not re-measured by the bench run
-K5_DRAM_TRAFFIC_C2 = (52.962304e6 + 3.445504e6) + (0.061184e6 + 0.0)
+# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch (the list-walk kernel) at config 2, from the
+# committed ncu --set full capture (profiles/r1c_k5_listwalk_c2.metrics.txt); not re-measured by the bench run
+K5_DRAM_TRAFFIC_C2 = 53.064192e6 + 5.001728e6
 BYTES_PER_SU_TICK = 200.0     # B_su
 BYTES_PER_PED_TICK = 200.0    # B_ped
 
@@ -423,7 +423,8 @@ def main():
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
-        "roofline": {"bound": "hbm", "kernel": "k-5 write-back (all k-5 kernels of a tick)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k-5 write-back (k5_listwalk_kernel at config 2; all k-5 kernels of a tick)",
+                     "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": K5_DRAM_TRAFFIC_C2 if args.workload == "c2" else None,
                      "peak_source": peak_src, "bytes_per_launch": BYTES_PER_SU_K5 * C,
