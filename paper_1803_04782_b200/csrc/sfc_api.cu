@@ -23,7 +23,7 @@ using namespace sfc;
 // own stream, so the CPU memcpy into pinned memory and the PCIe DMA overlap and add up across
 // lanes (a single cudaMemcpy from pageable memory is bound by one core's memcpy).
 struct Stager {
-    static constexpr int kLanes = 4;
+    static constexpr int kLanes = 8;
     static constexpr size_t kChunk = 4u << 20;
     void* pin[kLanes][2] = {};
     bool busy[kLanes][2] = {};

@@ -529,24 +529,24 @@ void Engine::verify_state(const SimState& s) const {
     OccupancyGrid expected(geom_);
     for (std::size_t i = 0; i < s.pedestrians.size(); ++i) {
         const Pedestrian& p = s.pedestrians[i];
-        const std::string who = "pedestrian " + std::to_string(p.id);
+        const auto who = [&p] { return "pedestrian " + std::to_string(p.id); }; // (only built for a rejection)
         if (p.id != static_cast<std::int32_t>(i)) reject("pedestrian ids must equal their index");
         const auto normal = wrap(geom_, p.center);
-        if (!normal || *normal != p.center) reject(who + " center not normalized");
-        if (p.walk_period < 1 || p.walk_phase < 0 || p.walk_phase >= p.walk_period) reject(who + " walk gate out of range");
-        if (p.goal_sect < 0 || p.goal_sect >= kSects) reject(who + " goal sect out of range");
+        if (!normal || *normal != p.center) reject(who() + " center not normalized");
+        if (p.walk_period < 1 || p.walk_phase < 0 || p.walk_phase >= p.walk_period) reject(who() + " walk gate out of range");
+        if (p.goal_sect < 0 || p.goal_sect >= kSects) reject(who() + " goal sect out of range");
         for (int k = 0; k < kDynKinds; ++k) {
             const FieldSpec& have = p.dyn_fields[static_cast<std::size_t>(k)];
             const FieldSpec& want = field_templates_[static_cast<std::size_t>(k)];
             if (have.kind != want.kind || have.geometry != want.geometry || have.gain != want.gain ||
                 have.decay != want.decay)
-                reject(who + " field spec does not match the engine template");
+                reject(who() + " field spec does not match the engine template");
         }
         const FootprintCells body = footprint_cells(geom_, p.center, p.footprint);
-        if (body.clipped) reject(who + " footprint crosses a closed edge");
+        if (body.clipped) reject(who() + " footprint crosses a closed edge");
         for (const SuIndex su : body.cells) {
             if (!expected.empty_at(su)) {
-                if (expected.at(su) == p.id) reject(who + " footprint wraps onto itself");
+                if (expected.at(su) == p.id) reject(who() + " footprint wraps onto itself");
                 reject("pedestrians " + std::to_string(expected.at(su)) + " and " + std::to_string(p.id) +
                        " overlap at su (" + std::to_string(su.x) + "," + std::to_string(su.y) + ")");
             }
@@ -555,6 +555,7 @@ void Engine::verify_state(const SimState& s) const {
     }
     const auto& got = s.occupancy.raw();
     const auto& want = expected.raw();
+    if (got.size() == want.size() && std::memcmp(got.data(), want.data(), got.size() * sizeof(got[0])) == 0) return;
     for (std::size_t i = 0; i < got.size(); ++i) {
         if (got[i] == want[i]) continue;
         const std::size_t w = static_cast<std::size_t>(geom_.width);
