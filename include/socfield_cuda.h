@@ -149,7 +149,13 @@ void sfc_error_detail(const sfc_engine* e, int64_t* tick, int32_t* phase, int32_
                       int32_t* su_y, double* value);
 
 /* Host -> device copy of a whole SimState; device -> host copy of what a tick mutates
- * (occupancy, dynamic images, centres, tick).  Engine::tick / Engine::run entry and exit. */
+ * (occupancy, dynamic images, centres, tick).  Engine::tick / Engine::run entry and exit.
+ *
+ * sfc_upload with the dense arrays NULL (occupancy, static_image, all three dyn_images) describes a
+ * freshly seeded population: the device then derives the occupancy grid from the footprints and
+ * rasterises the dynamic images itself, exactly as seed_population does (scenario.cpp:392-429),
+ * with a zero static image — no whole-grid host state is needed (a 32768^2 SimState is 141 GB).
+ * sfc_download skips every array that is NULL (e.g. only center_xy set: positions alone). */
 int sfc_upload(sfc_engine* e, const sfc_state_view* view);
 int sfc_download(sfc_engine* e, sfc_state_view* view);
 

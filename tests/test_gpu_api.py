@@ -387,3 +387,34 @@ def test_c4_replica_sparse_paths_agree(monkeypatch):
     assert np.array_equal(occ[prev[:, 1], prev[:, 0]], np.arange(n))
     for kind in ("dir-attractive", "dir-repulsive", "recurrent-repulsive"):
         assert np.array_equal(sa.image(kind).view(np.uint32), sb.image(kind).view(np.uint32)), kind
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["default", "window", "scatter", "scatter-gather-all"])
+def test_kinds_with_different_field_geometries(product_lib, monkeypatch, path):
+    """The Engine takes one FieldSpec per kind (engine.hpp:144-145) and they need not share a
+    geometry — only the scenario format ties them together.  Kinds with different supports cannot
+    share contributor lists (no list walk, no combined gating word): every k-5 path must fall back to
+    its general form and still match the oracle bit for bit."""
+    if path != "default":
+        monkeypatch.setenv("SFC_K5_PATH", path.split("-")[0])
+    if path == "scatter-gather-all":
+        monkeypatch.setenv("SFC_K5_EVENT_MAX", "0")
+    templates = [(7, 7, 1.0, -0.5), (5, 9, 1.3, -0.4), (9, 5, 0.8, -0.6)]
+    rng = np.random.default_rng(5)
+    w, h = 61, 43
+    cells = rng.choice(w * h, size=260, replace=False)
+    peds = [dict(x=int(c % w), y=int(c // w), goal=int(rng.integers(8)), period=int(p), phase=int(rng.integers(p)))
+            for c, p in zip(cells, rng.integers(1, 4, size=260))]
+    cfg = dict(goal_bias=1.0, rebuild_interval=7)
+    gpu = shim.Sim.from_arrays(product_lib, w, h, peds, cfg=shim.quiet_config(**cfg), templates=templates)
+    cpu = oracle.OracleSim.from_arrays(oracle.make_config(w, h, templates=templates, **cfg), peds)
+    total = 0
+    for _ in range(5):
+        moved = cpu.run(6)
+        np.testing.assert_array_equal(gpu.run(6), moved)
+        total += int(moved.sum())
+        same(gpu, cpu)
+        for k in range(3):
+            np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)))
+    assert total > 500  # the crowd really moves
