@@ -62,19 +62,18 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
 
     const int n = a.w.n;
     float* const tot = reinterpret_cast<float*>(smem_raw);                          // [kind * 8 + sect][kThreads]
-    double* const s_mag = reinterpret_cast<double*>(tot + kKinds * kSects * kThreads); // [kind][n]
-    uint32_t* const s_meta = reinterpret_cast<uint32_t*>(s_mag + (LIST_SMEM ? kKinds * n : 0));
-    uint32_t* const s_masks = s_meta + (LIST_SMEM ? n : 0);
-    long long* const rowoff = reinterpret_cast<long long*>(s_masks + (LIST_SMEM ? ((n + 1) & ~1) : 0)); // [rh]
+    double* const s_mag = reinterpret_cast<double*>(tot + kKinds * kSects * kThreads); // [n][4]: kinds 0..2 (+ pad): one 16 B + one 8 B load
+    int2* const s_ent = reinterpret_cast<int2*>(s_mag + (LIST_SMEM ? 4 * n : 0));    // [n] (cell offset dy * pitch + dx, masks)
+    long long* const rowoff = reinterpret_cast<long long*>(s_ent + (LIST_SMEM ? n : 0)); // [rh]
     // per region cell: one-hot orientation selectors of the event that left it (.x) / arrived at it (.y),
     // per kind in the byte lanes of the mask words (kind 2 is non-directional: orientation 0); 0 = no event
     uint2* const sel = reinterpret_cast<uint2*>(rowoff + a.rh);                      // [rh][rwp]
     if (LIST_SMEM) {
         for (int i = tid; i < n; i += kThreads) {
             const uint32_t m = a.w.meta[i];
-            s_meta[i] = (uint32_t)(((int)((m >> 8) & 0xFFu) - 128) * a.rwp + ((int)(m & 0xFFu) - 128)); // cell offset dy * pitch + dx
-            s_masks[i] = a.w.masks[i];
-            for (int k = 0; k < kKinds; ++k) s_mag[k * n + i] = a.w.mag[k * n + i];
+            s_ent[i] = make_int2(((int)((m >> 8) & 0xFFu) - 128) * a.rwp + ((int)(m & 0xFFu) - 128), (int)a.w.masks[i]);
+            for (int k = 0; k < kKinds; ++k) s_mag[4 * i + k] = a.w.mag[k * n + i];
+            s_mag[4 * i + 3] = 0.0;
         }
     }
 
@@ -175,22 +174,34 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
                 for (int u = 0; u < K / 2; ++u) { // list position j0 + u: term idx 2u (left), 2u + 1 (arrived) mod K
                     const int j = j0 + u;
                     if (j >= j_end) break; // uniform
-                    int off; // cell offset of the contributor: centre offset = mover - target
+                    int off;      // cell offset of the contributor: centre offset = mover - target
+                    uint32_t mk;  // orientation mask of kind k in byte k
                     if (LIST_SMEM) {
-                        off = (int)s_meta[j];
+                        const int2 ent = s_ent[j];
+                        off = ent.x;
+                        mk = (uint32_t)ent.y;
                     } else {
                         const uint32_t m = __ldg(a.w.meta + j);
                         off = ((int)((m >> 8) & 0xFFu) - 128) * RWP + ((int)(m & 0xFFu) - 128);
+                        mk = __ldg(a.w.masks + j);
                     }
                     const uint2 c = valid ? centre[off] : make_uint2(0u, 0u);
                     if (__ballot_sync(0xFFFFFFFFu, (c.x | c.y) != 0u) == 0u) continue; // zero terms never change a partial
-                    const uint32_t mk = LIST_SMEM ? s_masks[j] : __ldg(a.w.masks + j); // orientation mask of kind k in byte k
                     const uint32_t fbits = mk & c.x, tbits = mk & c.y; // gating the six terms is two ANDs
+                    double mg[kKinds];
+                    if (LIST_SMEM) {
+                        const double2 m01 = *reinterpret_cast<const double2*>(s_mag + 4 * j);
+                        mg[0] = m01.x;
+                        mg[1] = m01.y;
+                        mg[2] = s_mag[4 * j + 2];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < kKinds; ++k) mg[k] = __ldg(a.w.mag + k * n + j);
+                    }
 #pragma unroll
                     for (int k = 0; k < kKinds; ++k) {
-                        const double mg = LIST_SMEM ? s_mag[k * n + j] : __ldg(a.w.mag + k * n + j);
-                        add_if(p[k][2 * u], -mg, fbits & (0xFFu << (8 * k)));
-                        add_if(p[k][2 * u + 1], mg, tbits & (0xFFu << (8 * k)));
+                        add_if(p[k][2 * u], -mg[k], fbits & (0xFFu << (8 * k)));
+                        add_if(p[k][2 * u + 1], mg[k], tbits & (0xFFu << (8 * k)));
                     }
                 }
             }
@@ -238,8 +249,7 @@ LwShape lw_shape(const WalkLists& w) {
     s.rh = kMarkTileH + 2 * w.hh;
     s.list_smem = w.n <= kListSmemMax;
     size_t b = sizeof(float) * kKinds * kSects * kThreads;
-    if (s.list_smem) b += sizeof(double) * kKinds * w.n + sizeof(uint32_t) * (w.n + ((w.n + 1) & ~1));
-    b = (b + 7) & ~(size_t)7;
+    if (s.list_smem) b += sizeof(double) * 4 * w.n + sizeof(int2) * w.n;
     b += sizeof(long long) * s.rh;
     b += sizeof(uint2) * (size_t)s.rwp * s.rh;
     s.smem = (b + 15) & ~(size_t)15;
