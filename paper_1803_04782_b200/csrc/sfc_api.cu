@@ -82,6 +82,7 @@ struct sfc_engine {
     WalkLists walk{};        // merged contributor lists of the list-walk kernel (meta == nullptr: not available)
     int k5_listwalk = 1;     // dense tiles: list-walk kernel (SFC_K5_DENSE=gather: the event-walk gather)
     int k5_listwalk_only = 0; // the list-walk kernel alone (chosen in sfc_upload, or SFC_K5_PATH=listwalk)
+    int k5_list_cap = 0;      // SFC_K5_LIST_CAP: forces the large-field gather off its one-list path (tests)
     int k5_path_pref = -1;    // SFC_K5_PATH: 0 scatter, 1 window, 2 listwalk, -1 by crowd and field (sfc_upload)
     int sm_count = 148;
     Stager stager;
@@ -392,6 +393,7 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.walk = e->walk;
     l.listwalk = e->k5_listwalk;
     l.listwalk_only = e->k5_listwalk_only;
+    l.list_cap = e->k5_list_cap;
     return l;
 }
 
@@ -488,6 +490,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         e->k5_window_pref = path == "window";
     }
     if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
+    if (const char* knob = std::getenv("SFC_K5_LIST_CAP")) e->k5_list_cap = std::atoi(knob);
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;

@@ -231,6 +231,7 @@ struct K5Launch {
     WalkLists walk;      // k-5: merged contributor lists (meta == nullptr: the kinds do not share them)
     int listwalk;        // k-5: dense tiles go to the list-walk kernel (1) or the event-walk gather (0)
     int listwalk_only;   // k-5: the list-walk kernel is the only k-5 kernel (every / every active tile)
+    int list_cap;        // k-5 gather: events one appended list may hold (0: its capacity; tests lower it)
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);

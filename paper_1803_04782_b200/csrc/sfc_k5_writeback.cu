@@ -72,6 +72,7 @@ struct K5Args {
     int tiles_x;
     int advance_tick;
     int cap;          // cells staged per pass = event-list capacity
+    int list_cap;     // events one list may hold when chunks are appended (<= cap; SFC_K5_LIST_CAP lowers it for tests)
     int rw_max;       // region columns for a full tile
     int tab_smem;     // contributor tables fit in shared memory
     int part_doubles; // size of the partial-sum / scatter region, in doubles
@@ -205,7 +206,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             }
         }
         __syncthreads();
-        if (append && cs[ncols] > a.cap) return -1; // uniform
+        if (append && cs[ncols] > a.list_cap) return -1; // uniform
         for (int rc = warp; rc < ncols; rc += NW) {
             int pos = cs[rc];
             if (cs[rc + 1] == pos) continue;
@@ -704,6 +705,7 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     a.tiles_x = (l.g.W + kTileW - 1) / kTileW;
     a.advance_tick = l.advance_tick;
     a.cap = sh.cap;
+    a.list_cap = l.list_cap > 0 && l.list_cap < sh.cap ? l.list_cap : sh.cap;
     a.rw_max = sh.rw_max;
     a.tab_smem = sh.tab_smem;
     a.part_doubles = sh.part_doubles;

@@ -71,5 +71,10 @@ EXTRA = {
     "sparse-periodic": "grid = 203x117\ndensity = 0.004\ndirections = eight\nwalk_period = 1..2\nseed = 61\nrebuild_interval = 12\n",
     "sparse-closed": "grid = 150x90\nboundary = closed\ndensity = 0.006\ndirections = four\nseed = 62\nrebuild_interval = 9\n",
     "sparse-field15": "grid = 160x96\ndensity = 0.003\ndirections = eight\nfield_geometry = 15x11\nseed = 63\nrebuild_interval = 0\n",
+    # large fields: the region of a 32 x 16 k-5 tile exceeds one staging pass (chunked staging, one event list) ...
+    "field35": "grid = 97x83\ndensity = 0.03\ndirections = eight\nfield_geometry = 35x35\nwalk_period = 1..2\nseed = 71\n"
+               "rebuild_interval = 4\n",
+    # ... and, in a crowd, the events of a region overflow the list (per-walk re-staging)
+    "field41-crowd": "grid = 90x75\ndensity = 0.7\ndirections = eight\nfield_geometry = 41x41\nseed = 72\nrebuild_interval = 0\n",
     "wide-ragged": "grid = 131x67\ndensity = 0.3\ndirections = bi\nwalk_period = 1..3\nseed = 123\nrebuild_interval = 10\n",
 }

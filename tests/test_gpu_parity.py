@@ -170,3 +170,19 @@ def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path,
     for step in range(4):
         np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
         assert_state_equal(gpu, cpu, f"{name} {path} knob {knob} tick {8 * (step + 1)}")
+
+
+@pytest.mark.parametrize("name,ticks,list_cap", [("field35", 8, None), ("field41-crowd", 4, None), ("field35", 6, "16")])
+def test_large_field_gather(product_lib, monkeypatch, name, ticks, list_cap):
+    """Fields beyond 15 x 15 (BASELINE configs 3 and 5 use 35 x 35 and 77 x 77) take the event-walk
+    gather on 32 x 16 tiles whose field region is staged in column chunks: one sorted event list per
+    tile when the events fit, re-staging per walk when they do not (forced with a 16-event list).
+    Bit-identical to the oracle."""
+    if list_cap:
+        monkeypatch.setenv("SFC_K5_LIST_CAP", list_cap)
+    text = sc.EXTRA[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(2):
+        np.testing.assert_array_equal(gpu.run(ticks // 2), cpu.run(ticks // 2), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} tick {(step + 1) * (ticks // 2)}")
