@@ -179,10 +179,11 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, int code, int phase, int x
 // In slab mode the tiles whose field region reaches into the halo rows ("edge tiles") are not
 // listed — the neighbours' events arrive there as plain row copies — and are always processed.
 constexpr int kMarkTileW = 32, kMarkTileH = 8;
-constexpr unsigned kEpochPeriod = (1u << 20) - 1u; // stamps are erased once per period (sfc_run)
-constexpr unsigned kMarkCountMax = 0xFFFu;
+constexpr unsigned kEpochPeriod = (1u << 16) - 1u; // stamps are erased once per period (sfc_run)
+constexpr unsigned kMarkCountMax = 0xFFu;
 struct TileMarks {
-    unsigned* epoch; // [tiles_x * tiles_y] stamp << 12 | movers within reach (saturating), stamp = tick % period + 1
+    unsigned* epoch; // [tiles_x * tiles_y] stamp << 16 | blocks within reach << 8 | movers within reach (saturating);
+                     // stamp = tick % period + 1; block bit = 4 * (row of 8 x 4 blocks) + column
     int* list;       // [tiles_x * tiles_y]
     int tiles_x, tiles_y;
     int hw, hh;      // field reach (largest half extents over the three kinds)

@@ -200,11 +200,14 @@ __global__ void __launch_bounds__(kThreads, 3) k5_window_kernel(WinArgs a) {
         } else {
             tile = a.marks.list[titem - n_edge];
         }
-        if (a.use_list && titem >= n_edge) { // a listed tile: k-4 counted the movers within its reach
+        if (a.use_list && titem >= n_edge) { // a listed tile: k-4 counted the movers and noted the blocks within reach
             const unsigned word = a.marks.epoch[tile];
-            if ((word >> 12) == stamp && (int)(word & kMarkCountMax) > a.mover_max) { // dense: exact gather kernel
-                if (blk == 0 && lane == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
-                continue;
+            if ((word >> 16) == stamp) {
+                if (a.mover_max < (int)kMarkCountMax && (int)(word & kMarkCountMax) > a.mover_max) { // dense: exact kernel
+                    if (blk == 0 && lane == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
+                    continue;
+                }
+                if (!((word >> (8 + blk)) & 1u)) continue; // no mover's field box touches this block
             }
         }
         const int tile_y = tile / tiles_x, tile_x = tile - tile_y * tiles_x;

@@ -274,15 +274,24 @@ __device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m,
     for (int iy = 0; iy < nyr; ++iy)
         for (int ty = yr[iy][0] / kMarkTileH; ty <= yr[iy][1] / kMarkTileH; ++ty) {
             if (slab_active && (ty < m.edge_lo || ty >= m.edge_hi)) continue; // edge tiles are always processed
+            // rows of 8 x 4 blocks of this tile the reach rectangle touches (a tile is 2 block rows x 4 block columns)
+            const int by0 = (max(yr[iy][0], ty * kMarkTileH) - ty * kMarkTileH) >> 2;
+            const int by1 = (min(yr[iy][1], ty * kMarkTileH + kMarkTileH - 1) - ty * kMarkTileH) >> 2;
+            const unsigned rows = (by0 == 0 ? 0x0Fu : 0u) | (by1 == 1 ? 0xF0u : 0u);
             for (int ix = 0; ix < nxr; ++ix)
                 for (int tx = xr[ix][0] / kMarkTileW; tx <= xr[ix][1] / kMarkTileW; ++tx) {
+                    const int bx0 = (max(xr[ix][0], tx * kMarkTileW) - tx * kMarkTileW) >> 3;
+                    const int bx1 = (min(xr[ix][1], tx * kMarkTileW + kMarkTileW - 1) - tx * kMarkTileW) >> 3;
+                    const unsigned cols = ((2u << bx1) - (1u << bx0)) * 0x11u; // block columns bx0..bx1 in both block rows
+                    const unsigned blocks = rows & cols;
                     const int t = ty * m.tiles_x + tx;
-                    // stamp the tile and count this mover; the first mover of the tick lists the tile
+                    // stamp the tile, add its blocks within reach, count this mover; the first mover of the tick lists the tile
                     unsigned old = *reinterpret_cast<volatile unsigned*>(m.epoch + t);
                     for (;;) {
-                        const bool current = (old >> 12) == epoch;
+                        const bool current = (old >> 16) == epoch;
                         const unsigned n = current ? min((old & kMarkCountMax) + 1u, kMarkCountMax) : 1u;
-                        const unsigned prev = atomicCAS(m.epoch + t, old, (epoch << 12) | n);
+                        const unsigned b = (current ? (old >> 8) & 0xFFu : 0u) | blocks;
+                        const unsigned prev = atomicCAS(m.epoch + t, old, (epoch << 16) | (b << 8) | n);
                         if (prev == old) {
                             if (!current) m.list[atomicAdd(&ctl->active_count, 1)] = t;
                             break;
