@@ -75,10 +75,11 @@ WORKLOADS = {
         cells=32768 * 32768, peds=1000000, field=(7, 7), ticks_per_step=10, ref_ticks_per_step=1, resident=True),
     # BASELINE.json configs[4] "c5": 77x77 fields, linear regulation, dense crowd
     "c5": dict(
-        label="fine-resolution stress: 838 860 pedestrians, 4096x4096 su, rho 0.05, 77x77 fields, linear regulation r=3",
+        label="fine-resolution stress: 838 860 pedestrians, 4096x4096 su, rho 0.05, 77x77 fields, linear regulation r=3, "
+              "7x7 omni-repulsive obstacle fields on 1 % of the su",
         text="grid = 4096x4096\ndensity = 0.05\ndirections = eight\nfield_geometry = 77x77\nregulation = linear\n"
              "density_radius = 3\nseed = 42\nrebuild_interval = 0\n",
-        cells=4096 * 4096, peds=838860, field=(77, 77), ticks_per_step=2, ref_ticks_per_step=1),
+        cells=4096 * 4096, peds=838860, field=(77, 77), ticks_per_step=2, ref_ticks_per_step=1, obstacles=0.01),
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
@@ -186,6 +187,14 @@ def build_state(sf, w):
     state = sf.seed_population(cfg)
     if "exit" in w:  # c1: one omni-attractive field anchored at the exit, reaching the whole room
         state.set_static_fields([(sf.FieldSpec("omni-attractive", (399, 399), 1.0, -0.02), w["exit"])])
+    if "obstacles" in w:  # c5: dense obstacles = 7x7 omni-repulsive static fields on a seeded share of the su (seed 7)
+        import numpy as np
+
+        gw, gh = cfg.grid.width, cfg.grid.height
+        n = int(round(w["obstacles"] * gw * gh))
+        at = np.random.Generator(np.random.MT19937(7)).choice(gw * gh, size=n, replace=False)
+        spec = sf.FieldSpec("omni-repulsive", (7, 7), 1.0, -0.5)
+        state.set_static_fields([(spec, (int(a % gw), int(a // gw))) for a in at])
     return cfg, state
 
 
@@ -423,7 +432,8 @@ def main():
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
-        "roofline": {"bound": "hbm", "kernel": "k-5 write-back (k5_listwalk_kernel at config 2; all k-5 kernels of a tick)",
+        "roofline": {"bound": "hbm", "kernel": "k-5 write-back, all k-5 kernels of a tick (k5_listwalk_kernel alone at configs 1, 2 and the paper baseline; "
+                               "k5_window_kernel + dense hand-off at config 4; k5_writeback_kernel gather at configs 3, 5)",
                      "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": K5_DRAM_TRAFFIC_C2 if args.workload == "c2" else None,
