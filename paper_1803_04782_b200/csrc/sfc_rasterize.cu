@@ -133,23 +133,28 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     }
 
     float drift[kKinds] = {0.0f, 0.0f, 0.0f};
-    if (active) {
+    if (active) { // the su's 96-byte record as six 16-byte accesses
         const long long cell = cell_index(g, x0 + lx, y0 + ly);
-        if (a.mode == 0) {
-            float* rec = a.out + cell * 24;
+        float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + cell * 24);
+        if (a.mode == 1) {
+            float4 old[6];
 #pragma unroll
-            for (int q = 0; q < 24; ++q) rec[q] = acc[q * kRbThreads + tid];
-        } else if (a.mode == 1) {
-            const float* rec = a.dyn + cell * 24;
+            for (int v = 0; v < 6; ++v) old[v] = rec[v];
 #pragma unroll
-            for (int q = 0; q < 24; ++q) {
-                const float d = fabsf(rec[q] - acc[q * kRbThreads + tid]);
-                if (drift[q / 8] < d) drift[q / 8] = d; // std::max(worst, d): a NaN never wins
+            for (int v = 0; v < 6; ++v) {
+                const float o[4] = {old[v].x, old[v].y, old[v].z, old[v].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int q = 4 * v + c;
+                    const float d = fabsf(o[c] - acc[q * kRbThreads + tid]);
+                    if (drift[q / 8] < d) drift[q / 8] = d; // std::max(worst, d): a NaN never wins
+                }
             }
         } else {
-            float* rec = a.dyn + cell * 24;
 #pragma unroll
-            for (int q = 0; q < 24; ++q) rec[q] = acc[q * kRbThreads + tid];
+            for (int v = 0; v < 6; ++v)
+                rec[v] = make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
+                                     acc[(4 * v + 2) * kRbThreads + tid], acc[(4 * v + 3) * kRbThreads + tid]);
         }
     }
     if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
