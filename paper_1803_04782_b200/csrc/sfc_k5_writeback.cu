@@ -7,7 +7,13 @@
 // doubles through a K-slot StepCache (term idx -> slot idx mod K, accumulator.hpp:36-46), fold
 // the K slots in slot order, cast to float, add to the image.  6F mask probes per su.
 //
-// B200 formulation (bit-identical results).  A CTA owns a tile of 32 x 8 su.  It stages the tile +
+// This file holds two of the four bit-identical formulations (the list walk for small fields is
+// sfc_k5_listwalk.cu, the warp-per-block kernel for sparse crowds sfc_k5_window.cu) and the
+// dispatcher between them (launch_k5_writeback; the engine chooses in sfc_upload):
+// the SCATTER kernel for ordinary crowds on fields beyond 11 x 11, and the event-walk GATHER for
+// fields beyond 15 x 15 and for tiles the scatter finds crowded there.
+//
+// A CTA owns a tile of 32 x 8 su.  It stages the tile +
 // field-halo region of the 2-byte event map in shared memory once (coalesced row reads) and
 // compacts the (few) movement events into a list ordered by (x, then y) with warp ballots — no
 // atomics.  That order equals the reference's contributor-list order for every target in the
@@ -77,7 +83,6 @@ struct K5Args {
     int tab_smem;     // contributor tables fit in shared memory
     int part_doubles; // size of the partial-sum / scatter region, in doubles
     int ev_max;       // scatter handles tiles with at most this many events in reach
-    int debug_stop;   // profiling only (results invalid): leave the scatter kernel after phase N
     int n_tiles;      // tiles_x * tiles_y
     TileMarks marks;  // scatter kernel: active-tile list written by k-4 (epoch == nullptr: every tile)
 };
@@ -269,7 +274,6 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
         }
         __syncthreads();
         n_events = *n_list;
-        if (a.debug_stop == 7) return;
         if (n_events == 0) return; // nobody moved within reach of this tile
         if (n_events > a.ev_max) { // dense tile: hand it to the gather kernel
             if (tid == 0) a.dense_list[atomicAdd(&a.ctl->dense_count, 1)] = tile;
@@ -286,7 +290,6 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             }
             evl[rank] = mine;
         }
-        if (a.debug_stop == 1) return;
         // support offsets of the largest box, decoded once per CTA: (dx + 128) | (dy + 128) << 8
         const int BW = 2 * HW + 1, BOX = BW * (2 * HH + 1);
         for (int o = tid; o < BOX; o += NT) {
@@ -334,7 +337,6 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             if (tid == 0) *n_replay = 0;
         }
         __syncthreads();
-        if (a.debug_stop == 2) return;
         // threads take (event, support offset) pairs — evenly packed whatever the event count
         const int BW = 2 * HW + 1, BOX = BW * (2 * HH + 1);
         const int pairs = n_events * BOX;
@@ -382,7 +384,6 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             }
         }
         __syncthreads();
-        if (a.debug_stop == 3) return;
         // addresses with three or more terms: exact K-slot replay, one address per thread
         for (int cell = tid; cell < CELLS; cell += NT) {
             uint32_t m = seen3[cell];
@@ -441,7 +442,6 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
             acc[addr] = total;
         }
         __syncthreads();
-        if (a.debug_stop == 4) return;
         // apply: one 32-byte sector per touched (su, kind); every load of a thread is issued before
         // the first is consumed
         constexpr int PAIRS = (CELLS * kKinds + NT - 1) / NT;
@@ -614,7 +614,6 @@ __global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
     const int tid = threadIdx.x;
     if (MODE != kModeDense && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
     if (a.ctl->error_code != 0) return;
-    if (MODE == kModeScatter && a.debug_stop == 6) return;
     if (MODE == kModeDense && (int)blockIdx.x >= a.ctl->dense_count) return; // no dense tile for this CTA
     const Smem sm = carve(smem_raw, a);
     if (a.tab_smem) { // contributor tables: one copy per CTA
@@ -629,7 +628,6 @@ __global__ void __launch_bounds__(NT) k5_writeback_kernel(K5Args a) {
         }
     }
     if (MODE != kModeScatter) __syncthreads(); // (the scatter synchronises after its event collection, before any table use)
-    if (MODE == kModeScatter && a.debug_stop == 5) return;
     if constexpr (MODE == kModeDense) { // persistent over the tiles the scatter kernel declined
         const int n = a.ctl->dense_count;
         for (int i = blockIdx.x; i < n; i += gridDim.x) {
@@ -711,10 +709,6 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     a.part_doubles = sh.part_doubles;
     a.ev_max = l.ev_max;
     a.marks = (MODE == kModeScatter && kBlockH * ROWS == kMarkTileH) ? l.marks : TileMarks{};
-    {
-        static const int stop = std::getenv("SFC_K5_DEBUG_STOP") ? std::atoi(std::getenv("SFC_K5_DEBUG_STOP")) : 0;
-        a.debug_stop = stop;
-    }
     const int tiles_y = (l.g.rows + MH - 1) / MH;
     long long blocks = (long long)a.tiles_x * tiles_y;
     a.n_tiles = (int)blocks;
