@@ -410,7 +410,8 @@ def main():
         return 0
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        r = cpu_reference(w, REF_TICKS_PER_STEP, 8 if args.workload in ("c1", "c2") else 1, 1 if args.workload in ("c1", "c2") else 0)
+        # ~10 s of host work at config 2 (0.15 s per tick on 16 cores); the large configs take minutes per tick
+        r = cpu_reference(w, REF_TICKS_PER_STEP, 32 if args.workload in ("c1", "c2") else 1, 1 if args.workload in ("c1", "c2") else 0)
         cpu = {"value": r["value"], "unit": "pedestrian-steps/s", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
     line = {
         "metric": "pedestrian-steps/s", "value": value, "unit": "pedestrian-steps/s",
