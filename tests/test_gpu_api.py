@@ -418,3 +418,24 @@ def test_kinds_with_different_field_geometries(product_lib, monkeypatch, path):
         for k in range(3):
             np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)))
     assert total > 500  # the crowd really moves
+
+
+@pytest.mark.gpu
+def test_one_run_across_the_stamp_period(monkeypatch):
+    """A single run longer than the 65535-tick period of the active-tile stamps: without the periodic
+    erase a tile last listed exactly one period earlier would look already listed and be skipped.
+    The list-driven window path must end where the every-tile list walk ends."""
+    text = "grid = 96x64\ndensity = 0.004\ndirections = eight\nseed = 9\nrebuild_interval = 0\n"
+    cfg = sf.parse_scenario(text)
+    a_state, b_state = sf.seed_population(cfg), sf.seed_population(cfg)
+    monkeypatch.setenv("SFC_K5_PATH", "window")
+    a = sf.Engine(cfg)
+    monkeypatch.setenv("SFC_K5_PATH", "listwalk")
+    monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "0")
+    b = sf.Engine(cfg)
+    ticks = 65535 + 40
+    ma = a.run(a_state, ticks)
+    mb = b.run(b_state, ticks)
+    assert [m.moved for m in ma[-200:]] == [m.moved for m in mb[-200:]]
+    same, why = sf.states_identical(a_state, b_state)
+    assert same, why

@@ -186,3 +186,21 @@ def test_large_field_gather(product_lib, monkeypatch, name, ticks, list_cap):
     for step in range(2):
         np.testing.assert_array_equal(gpu.run(ticks // 2), cpu.run(ticks // 2), err_msg=f"{name} moved")
         assert_state_equal(gpu, cpu, f"{name} tick {(step + 1) * (ticks // 2)}")
+
+
+@pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list"])
+def test_tile_stamps_survive_the_epoch_period(product_lib, monkeypatch, path):
+    """The active-tile stamps carry the tick modulo 65535; the engine erases them once per period so
+    a stamp from exactly one period ago cannot pass for the current tick.  Run across the boundary
+    (and once more across it in a second run) with every list-driven k-5 path."""
+    monkeypatch.setenv("SFC_K5_PATH", path.split("-")[0])
+    if path.endswith("-list"):
+        monkeypatch.setenv("SFC_K5_ACTIVE_LIST", "1")
+    text = sc.variant(sc.EXTRA["sparse-periodic"], rebuild_interval=0)
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for start in (65531, 2 * 65535 - 3):
+        gpu.tick = cpu.tick = start
+        for _ in range(3):
+            np.testing.assert_array_equal(gpu.run(3), cpu.run(3))
+            assert_state_equal(gpu, cpu, f"{path} tick {gpu.tick}")
