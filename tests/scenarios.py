@@ -76,5 +76,8 @@ EXTRA = {
                "rebuild_interval = 4\n",
     # ... and, in a crowd, the events of a region overflow the list (per-walk re-staging)
     "field41-crowd": "grid = 90x75\ndensity = 0.7\ndirections = eight\nfield_geometry = 41x41\nseed = 72\nrebuild_interval = 0\n",
+    # 13 x 13 fields (168 offsets): beyond the list-walk-alone range, within the list walk's range as the dense kernel
+    "field13-crowd": "grid = 70x45\ndensity = 0.5\ndirections = eight\nfield_geometry = 13x13\nwalk_period = 1..2\nseed = 81\n"
+                     "rebuild_interval = 6\n",
     "wide-ragged": "grid = 131x67\ndensity = 0.3\ndirections = bi\nwalk_period = 1..3\nseed = 123\nrebuild_interval = 10\n",
 }

@@ -130,7 +130,7 @@ def test_against_compiled_reference(product_lib, ref_lib):
 
 @pytest.mark.parametrize("knob,dense", [("0", "gather"), ("100000", "gather"), ("3", "gather"), ("3", "listwalk")])
 @pytest.mark.parametrize("name", ["desk64", "k2", "k4", "k16", "field-5x9", "field-bigger-than-grid", "closed-four",
-                                  "wide-ragged", "d0.1-eight-ped1", "d0.9-four-ped3"])
+                                  "wide-ragged", "d0.1-eight-ped1", "d0.9-four-ped3", "field13-crowd"])
 def test_both_k5_formulations(product_lib, monkeypatch, name, knob, dense):
     """The scatter path of k-5 chooses per tile by the number of movers in reach: an event-centric
     scatter (sparse tiles) or a dense kernel — the event-walk gather or the list walk.
@@ -170,6 +170,16 @@ def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path,
     for step in range(4):
         np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
         assert_state_equal(gpu, cpu, f"{name} {path} knob {knob} tick {8 * (step + 1)}")
+
+
+def test_default_path_field13(product_lib):
+    """13 x 13 fields in a crowd, no knobs: scatter kernel, crowded tiles handed to the list walk."""
+    text = sc.EXTRA["field13-crowd"]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(3):
+        np.testing.assert_array_equal(gpu.run(5), cpu.run(5))
+        assert_state_equal(gpu, cpu, f"field13 tick {5 * (step + 1)}")
 
 
 @pytest.mark.parametrize("name,ticks,list_cap", [("field35", 8, None), ("field41-crowd", 4, None), ("field35", 6, "16")])
