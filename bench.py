@@ -422,6 +422,7 @@ def main():
         "data": "synthetic (seeded scenario, seed 42)",
         "config": {"workload": w["label"], "ticks_per_step": TICKS_PER_STEP, "cells": C, "pedestrians": P,
                    "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+                   "k5_path": c1.get("k5_path"), "k5_active_list": c1.get("k5_active_list"),
                    "l2": f"no flush: the tick re-touches its whole working set ({134 * C / 1e6:.0f} MB: images, static image, "
                          "occupancy, events) against a 126 MB L2; k-5 only touches su within reach of a mover, so "
                          "roofline.traffic (DRAM bytes actually moved, ncu) is far below the algorithmic bytes"},

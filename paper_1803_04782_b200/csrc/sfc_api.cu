@@ -1267,7 +1267,11 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
     return status;
 }
 
-void sfc_get_counters(const sfc_engine* e, sfc_counters* out) { *out = e->counters; }
+void sfc_get_counters(const sfc_engine* e, sfc_counters* out) {
+    *out = e->counters;
+    out->k5_path = e->k5_listwalk_only ? 2 : (e->k5_window ? 1 : 0);
+    out->k5_active_list = e->marks.epoch != nullptr;
+}
 
 double sfc_last_run_ms(const sfc_engine* e) { return e->last_run_ms; }
 
