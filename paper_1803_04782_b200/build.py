@@ -29,7 +29,7 @@ HOST = os.path.join(PKG, "host")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 
-CUDA_SOURCES = ["sfc_api.cu", "sfc_ped_kernels.cu", "sfc_k5_writeback.cu", "sfc_k5_window.cu", "sfc_k5_listwalk.cu", "sfc_rasterize.cu", "sfc_slab.cu"]
+CUDA_SOURCES = ["sfc_api.cu", "sfc_ped_kernels.cu", "sfc_k5_writeback.cu", "sfc_k5_window.cu", "sfc_k5_listwalk.cu", "sfc_k5_pairs.cu", "sfc_rasterize.cu", "sfc_slab.cu"]
 HOST_SOURCES = ["model.cpp", "engine.cpp", "raster.cpp", "scenario.cpp"]
 
 NVCC_FLAGS = [
@@ -66,8 +66,22 @@ def build_cuda(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(LIB, exist_ok=True)
     target = os.path.join(LIB, "libsocfield_cuda.so")
     sources = [os.path.join(CSRC, s) for s in CUDA_SOURCES]
-    if force or _newer(target, sources + _headers()):
-        _run([NVCC, *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-shared", "-o", target, *sources], verbose)
+    # one object per translation unit (only the changed ones are recompiled, in parallel), then link
+    objdir = os.path.join(LIB, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objects, stale = [], []
+    for src in sources:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objects.append(obj)
+        if force or _newer(obj, [src] + _headers()):
+            stale.append([NVCC, *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-c", "-o", obj, src])
+    if stale:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=min(len(stale), os.cpu_count() or 1)) as pool:
+            list(pool.map(lambda cmd: _run(cmd, verbose), stale))
+    if stale or _newer(target, objects):
+        _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target, *objects], verbose)
     return target
 
 

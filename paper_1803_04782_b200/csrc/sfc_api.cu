@@ -83,7 +83,10 @@ struct sfc_engine {
     int k5_listwalk = 1;     // dense tiles: list-walk kernel (SFC_K5_DENSE=gather: the event-walk gather)
     int k5_listwalk_only = 0; // the list-walk kernel alone (chosen in sfc_upload, or SFC_K5_PATH=listwalk)
     int k5_list_cap = 0;      // SFC_K5_LIST_CAP: forces the large-field gather off its one-list path (tests)
-    int k5_path_pref = -1;    // SFC_K5_PATH: 0 scatter, 1 window, 2 listwalk, -1 by crowd and field (sfc_upload)
+    int k5_path_pref = -1;    // SFC_K5_PATH: 0 scatter, 1 window, 2 listwalk, 3 pairs, -1 by crowd and field (sfc_upload)
+    PairTables pairs{};       // tables of the pair kernel (blob == nullptr: the field geometry does not fit it)
+    int k5_pairs = 0;         // the pair kernel is the k-5 kernel (chosen in sfc_upload)
+    int pairs_ctas = 148;
     int sm_count = 148;
     Stager stager;
     bool uploaded = false;
@@ -160,6 +163,7 @@ void free_peds(sfc_engine* e) {
 
 int ensure_peds(sfc_engine* e, long long n) {
     if (n <= e->ped_capacity && e->peds.center) {
+        if (n != e->peds.n) e->graph_valid = false; // the captured tick holds the population size (grid sizes, PedArrays::n)
         e->peds.n = n;
         return SFC_OK;
     }
@@ -394,6 +398,9 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.listwalk = e->k5_listwalk;
     l.listwalk_only = e->k5_listwalk_only;
     l.list_cap = e->k5_list_cap;
+    l.pairs = e->pairs;
+    l.pairs_path = e->k5_pairs;
+    l.pairs_ctas = e->pairs_ctas;
     return l;
 }
 
@@ -486,7 +493,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
         const std::string path(knob);
-        e->k5_path_pref = path == "window" ? 1 : (path == "listwalk" ? 2 : 0);
+        e->k5_path_pref = path == "window" ? 1 : (path == "listwalk" ? 2 : (path == "pairs" ? 3 : 0));
         e->k5_window_pref = path == "window";
     }
     if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
@@ -551,6 +558,17 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
             e->walk.hh = h.hh;
             std::memcpy(e->walk.start, h.start, sizeof h.start);
             std::memcpy(e->walk.sect_of, h.sect_of, sizeof h.sect_of);
+            std::vector<unsigned char> blob;
+            PairTables pt{};
+            if (build_pair_tables(h, cfg->chunk_k, &pt, &blob)) {
+                unsigned char* dev = nullptr;
+                ok = dev_alloc(&dev, (long long)blob.size()) == cudaSuccess;
+                if (ok) e->table_allocs.push_back(dev);
+                ok = ok && cudaMemcpy(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+                if (!ok) return bail(fail(e, SFC_E_CUDA, "cudaMalloc / cudaMemcpy (pair tables)"));
+                pt.blob = dev;
+                e->pairs = pt;
+            }
         }
     }
 
@@ -628,6 +646,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     if (e->k5_tile_rows != kMarkTileH || !k5_listwalk_supported(e->walk)) e->k5_listwalk = 0; // (its tiles are 32 x 8)
     if (e->k5_window_ok)
         cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
+    if (e->k5_tile_rows != kMarkTileH) e->pairs.blob = nullptr;
+    if (e->pairs.blob) cu(prepare_k5_pairs(e->pairs, e->sm_count, &e->pairs_ctas), "cudaFuncSetAttribute(k5 pairs)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
     if (rc == SFC_OK) rc = ensure_peds(e, 0);
     if (rc == SFC_OK) rc = ensure_moved(e, 1);
@@ -760,14 +780,16 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         //   else, fields up to 11 x 11   -> the list-walk kernel alone: per-su cost fixed by the field area, at or
         //                                   below the scatter kernel's from corridor densities up, far below for crowds
         //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
-        const int window = e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
-        const int walk_only = !window && e->k5_listwalk && (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
+        const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || e->k5_path_pref < 0);
+        const int window = !pairs && e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
+        const int walk_only = !pairs && !window && e->k5_listwalk && (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
         const bool use = window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse);
-        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only) {
+        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs) {
             e->marks = use ? m : TileMarks{};
             e->k5_window = window;
             e->k5_listwalk_only = walk_only;
-            e->k5_launches = walk_only ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
+            e->k5_pairs = pairs;
+            e->k5_launches = (walk_only || pairs) ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
             e->graph_valid = false;
         }
         // the tick counter may restart: forget every epoch stamp
@@ -1269,7 +1291,7 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
 
 void sfc_get_counters(const sfc_engine* e, sfc_counters* out) {
     *out = e->counters;
-    out->k5_path = e->k5_listwalk_only ? 2 : (e->k5_window ? 1 : 0);
+    out->k5_path = e->k5_pairs ? 3 : (e->k5_listwalk_only ? 2 : (e->k5_window ? 1 : 0));
     out->k5_active_list = e->marks.epoch != nullptr;
 }
 

@@ -213,6 +213,15 @@ struct WalkListsHost {
     int sect_of[kKinds][kSects] = {};
 };
 
+// Tables of the pair formulation of k-5 (sfc_k5_pairs.cu), one device blob: the row-bits ->
+// window-word lookup (t_bytes), then the 64 contributor entries.
+struct PairTables {
+    const unsigned char* blob;
+    long long t_bytes;
+    int fw, fh, hw, hh;
+    uint32_t sect_packed[kKinds]; // sect of kind k fed by sect group g in bits [3g, 3g + 3)
+};
+
 // ---- launchers (defined in the .cu files) --------------------------------------------------
 struct K5Launch {
     GridDev g;
@@ -233,6 +242,9 @@ struct K5Launch {
     int listwalk;        // k-5: dense tiles go to the list-walk kernel (1) or the event-walk gather (0)
     int listwalk_only;   // k-5: the list-walk kernel is the only k-5 kernel (every / every active tile)
     int list_cap;        // k-5 gather: events one appended list may hold (0: its capacity; tests lower it)
+    PairTables pairs;    // k-5: tables of the pair kernel (blob == nullptr: field not supported)
+    int pairs_path;      // k-5: the pair kernel is the k-5 kernel (every / every active tile)
+    int pairs_ctas;      // k-5: its persistent grid
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
@@ -291,6 +303,10 @@ bool build_walk_lists(const sfc_tables& t, WalkListsHost* out);
 bool k5_listwalk_supported(const WalkLists& w);
 cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count);
 cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& a, bool from_dense_list);
+// pair formulation of k-5 (sfc_k5_pairs.cu)
+bool build_pair_tables(const WalkListsHost& w, int chunk_k, PairTables* out, std::vector<unsigned char>* blob);
+cudaError_t prepare_k5_pairs(const PairTables& t, int sm_count, int* ctas);
+cudaError_t launch_k5_pairs(cudaStream_t s, const K5Launch& a);
 cudaError_t prepare_rebuild(const TablesDev& t);
 
 } // namespace sfc

@@ -148,7 +148,7 @@ def test_both_k5_formulations(product_lib, monkeypatch, name, knob, dense):
 
 
 @pytest.mark.parametrize("path,knob", [("window", None), ("window", "100000"), ("window", "2"), ("scatter-list", None),
-                                       ("listwalk", None), ("listwalk-list", None)])
+                                       ("listwalk", None), ("listwalk-list", None), ("pairs", None), ("pairs-list", None)])
 @pytest.mark.parametrize("name", ["desk64", "k2", "k16", "field-5x9", "field21", "field-bigger-than-grid", "closed-four",
                                   "closed-ped3", "ped5", "wide-ragged", "sparse-periodic", "sparse-closed", "sparse-field15",
                                   "d0.9-four-ped3"])
@@ -158,6 +158,7 @@ def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path,
     replay).  Forced here on crowds of every density: the window kernel with its default hand-off
     to the dense gather, with every tile kept (knob 100000) or nearly every tile handed off (2), and
     the scatter kernel driven from the list, the list-walk kernel alone over every tile and over the
+    listed tiles, the pair kernel (default for fields up to 9 su wide) over every tile and over the
     listed tiles.  All bit-identical to the oracle."""
     monkeypatch.setenv("SFC_K5_PATH", path.split("-")[0])
     if path.endswith("-list"):
@@ -198,7 +199,7 @@ def test_large_field_gather(product_lib, monkeypatch, name, ticks, list_cap):
         assert_state_equal(gpu, cpu, f"{name} tick {(step + 1) * (ticks // 2)}")
 
 
-@pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list"])
+@pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list", "pairs-list"])
 def test_tile_stamps_survive_the_epoch_period(product_lib, monkeypatch, path):
     """The active-tile stamps carry the tick modulo 65535; the engine erases them once per period so
     a stamp from exactly one period ago cannot pass for the current tick.  Run across the boundary
