@@ -5,6 +5,7 @@
 // There is no CPU path: without a CUDA device sfc_create fails with SFC_E_NO_DEVICE.
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -86,7 +87,10 @@ struct sfc_engine {
     int k5_path_pref = -1;    // SFC_K5_PATH: 0 scatter, 1 window, 2 listwalk, 3 pairs, -1 by crowd and field (sfc_upload)
     PairTables pairs{};       // tables of the pair kernel (blob == nullptr: the field geometry does not fit it)
     int k5_pairs = 0;         // the pair kernel is the k-5 kernel (chosen in sfc_upload)
-    int pairs_ctas = 148;
+    int pairs_ctas[2] = {148, 148};
+    int pairs_red = 0;        // its RED variant is exact for the uploaded state (sfc_upload)
+    int pairs_red_tables = 0; // ... as far as the field magnitudes go (all >= 2^-40: sums are multiples of 2^-115)
+    int pairs_red_pref = -1;  // SFC_K5_RED: 0 never, 1 always (tests), -1 when provably exact
     int sm_count = 148;
     Stager stager;
     bool uploaded = false;
@@ -400,7 +404,9 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.list_cap = e->k5_list_cap;
     l.pairs = e->pairs;
     l.pairs_path = e->k5_pairs;
-    l.pairs_ctas = e->pairs_ctas;
+    l.pairs_ctas[0] = e->pairs_ctas[0];
+    l.pairs_ctas[1] = e->pairs_ctas[1];
+    l.pairs_red = e->pairs_red;
     return l;
 }
 
@@ -498,6 +504,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     }
     if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
     if (const char* knob = std::getenv("SFC_K5_LIST_CAP")) e->k5_list_cap = std::atoi(knob);
+    if (const char* knob = std::getenv("SFC_K5_RED")) e->pairs_red_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
@@ -558,6 +565,9 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
             e->walk.hh = h.hh;
             std::memcpy(e->walk.start, h.start, sizeof h.start);
             std::memcpy(e->walk.sect_of, h.sect_of, sizeof h.sect_of);
+            e->pairs_red_tables = 1;
+            for (double m : h.mag)
+                if (!(std::fabs(m) >= 0x1p-40 && std::fabs(m) <= 0x1p40)) e->pairs_red_tables = 0;
             std::vector<unsigned char> blob;
             PairTables pt{};
             if (build_pair_tables(h, cfg->chunk_k, &pt, &blob)) {
@@ -647,7 +657,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     if (e->k5_window_ok)
         cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
     if (e->k5_tile_rows != kMarkTileH) e->pairs.blob = nullptr;
-    if (e->pairs.blob) cu(prepare_k5_pairs(e->pairs, e->sm_count, &e->pairs_ctas), "cudaFuncSetAttribute(k5 pairs)");
+    if (e->pairs.blob) cu(prepare_k5_pairs(e->pairs, e->sm_count, e->pairs_ctas), "cudaFuncSetAttribute(k5 pairs)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
     if (rc == SFC_OK) rc = ensure_peds(e, 0);
     if (rc == SFC_OK) rc = ensure_moved(e, 1);
@@ -724,6 +734,10 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         attr[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
     }
     const long long W = e->g.W;
+    Ctl h{};
+    h.tick = v->tick;
+    h.run_base = v->tick;
+    SFC_CUDA(cudaMemcpyAsync(e->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, e->stream)); // (h lives until the sync below)
     // A view without the dense arrays (occupancy / images NULL) describes a freshly seeded
     // population: the device derives them itself below (no whole-grid host state needed).
     if (!v->occupancy) SFC_CUDA(cudaMemsetAsync(e->occ, 0xFF, sizeof(int) * (size_t)C, e->stream));
@@ -743,7 +757,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
             for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
                 const long long n = std::min(e->stage_cells, n_seg - c0);
                 SFC_CUDA(bulk_copy(e, e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects, true));
-                SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, dc + c0, n));
+                SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, dc + c0, n, e->ctl));
                 e->counters.kernel_launches += 1;
                 e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
             }
@@ -795,15 +809,20 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         // the tick counter may restart: forget every epoch stamp
         SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(unsigned) * (size_t)n_tiles, e->stream));
     }
-    Ctl h{};
-    h.tick = v->tick;
-    h.run_base = v->tick;
-    SFC_CUDA(cudaMemcpyAsync(e->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, e->stream));
     if (!v->occupancy && P > 0) { // seed_population, scenario.cpp:424
         SFC_CUDA(launch_occupancy_from_peds(e->stream, e->g, e->peds, e->occ));
         e->counters.kernel_launches += 1;
     }
+    int tiny = 0;
+    SFC_CUDA(cudaMemcpyAsync(&tiny, &e->ctl->tiny_image, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
     SFC_CUDA(cudaStreamSynchronize(e->stream)); // gate/attr staging vectors die here
+    {   // float reductions at the L2 flush subnormals: exact only while no image value can be one
+        const int red = e->pairs_red_pref >= 0 ? e->pairs_red_pref : (e->pairs_red_tables && !tiny);
+        if (red != e->pairs_red) {
+            e->pairs_red = red;
+            e->graph_valid = false;
+        }
+    }
     e->tick = v->tick;
     e->uploaded = true;
     if (!v->dyn_images[0] || !v->dyn_images[1] || !v->dyn_images[2]) { // rasterize_dynamic, scenario.cpp:427

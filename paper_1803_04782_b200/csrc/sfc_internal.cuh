@@ -136,6 +136,8 @@ struct Ctl {
     int halo_counts[4];      // slab mode: records packed per (edge, kind): [edge*2 + kind]
     int active_count;        // k-5: tiles within reach of this tick's movers (TileMarks::list), reset by k-3
     unsigned int epoch;      // k-5: this tick's tile stamp (set by k-3, read by k-4 and k-5; never 0)
+    int tiny_image;          // upload: an uploaded dynamic-image value is non-zero below 2^-92 — sums could be
+                             // subnormal, so k-5 may not use flush-to-zero float reductions (sfc_k5_pairs.cu)
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -244,7 +246,8 @@ struct K5Launch {
     int list_cap;        // k-5 gather: events one appended list may hold (0: its capacity; tests lower it)
     PairTables pairs;    // k-5: tables of the pair kernel (blob == nullptr: field not supported)
     int pairs_path;      // k-5: the pair kernel is the k-5 kernel (every / every active tile)
-    int pairs_ctas;      // k-5: its persistent grid
+    int pairs_ctas[2];   // k-5: its persistent grid ([1]: the RED variant)
+    int pairs_red;       // k-5: image += (float)total as a float reduction at the L2 (no image value can be subnormal)
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
@@ -285,7 +288,7 @@ cudaError_t launch_dbg_vote(cudaStream_t s, const DebugArrays& d, int fault_inve
 
 // layout conversion between the host's per-kind images and the interleaved record buffer
 cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, int kind, long long cells_begin,
-                              long long cells);
+                              long long cells, Ctl* ctl);
 cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
                                 long long cells);
 cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v);

@@ -91,12 +91,15 @@ __device__ __forceinline__ void add_if(double& p, double t, uint32_t flag) { // 
 }
 
 // one-hot orientation selectors of an event byte, per kind in the byte lanes (kind 2 is non-directional)
-__device__ __forceinline__ uint32_t selector(uint32_t b) {
-    return (b & 0x80u) ? ((1u << (b & 7u)) | (256u << ((b >> 3) & 7u)) | 0x10000u) : 0u;
+__device__ __forceinline__ uint32_t selector(uint32_t b) { // (branch-free: 0 when bit 7 is clear)
+    return ((1u << (b & 7u)) | (256u << ((b >> 3) & 7u)) | 0x10000u) * (b >> 7);
 }
 
-template <int PASSES> // staging passes: (4 + 2 hh) / 2 region-row pairs
-__global__ void __launch_bounds__(kThreads) k5_pairs_kernel(PairArgs a) {
+// PASSES: staging passes, (4 + 2 hh) / 2 region-row pairs.  RED: image += (float)total as a
+// fire-and-forget float reduction at the L2 (round-to-nearest like the reference's add; it flushes
+// subnormals, so the engine only selects it when no image value can be subnormal — sfc_upload).
+template <int PASSES, bool RED>
+__global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
@@ -175,6 +178,11 @@ __global__ void __launch_bounds__(kThreads) k5_pairs_kernel(PairArgs a) {
         return false;
     };
 
+    // image += (float)total is a read-modify-write of a value nobody else touches: the load is
+    // issued when a pair's totals are known and consumed one pair later, behind that pair's work
+    float* pend_at[kKinds] = {nullptr, nullptr, nullptr};
+    float pend_old[kKinds] = {0.f, 0.f, 0.f}, pend_add[kKinds] = {0.f, 0.f, 0.f};
+
     int x0 = 0, y0 = 0, nx0 = 0, ny0 = 0;
     uint32_t code[PASSES], next_code[PASSES];
     bool have = fetch(x0, y0, code);
@@ -184,10 +192,13 @@ __global__ void __launch_bounds__(kThreads) k5_pairs_kernel(PairArgs a) {
         uint32_t rows_nz = 0u;
 #pragma unroll
         for (int p = 0; p < PASSES; ++p) {
-            if (code[p]) ws->sel[(2 * p + r0) * kPitch + c] = make_uint2(selector(code[p] & 0xFFu), selector(code[p] >> 8));
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, code[p] != 0u);
+            if (bal != 0u) { // (warp-uniform)
+                if (code[p]) ws->sel[(2 * p + r0) * kPitch + c] = make_uint2(selector(code[p] & 0xFFu), selector(code[p] >> 8));
+                if (bal & 0xFFFFu) rows_nz |= 1u << (2 * p);
+                if (bal >> 16) rows_nz |= 2u << (2 * p);
+            }
             if (lane == 0) *reinterpret_cast<uint32_t*>(&ws->rb[2 * p]) = bal;
-            rows_nz |= ((bal & 0xFFFFu) ? 1u : 0u) << (2 * p) | ((bal >> 16) ? 2u : 0u) << (2 * p);
         }
         const int bx0 = x0, by0 = y0;
         have = fetch(nx0, ny0, next_code); // the next block's loads fly while this one is processed
@@ -271,11 +282,19 @@ __global__ void __launch_bounds__(kThreads) k5_pairs_kernel(PairArgs a) {
                 float* const rec = rec0 + (uy * g.W + ux) * (kKinds * kSects);
 #pragma unroll
                 for (int k = 0; k < kKinds; ++k) {
+                    if (!RED && pend_at[k]) *pend_at[k] = __fadd_rn(pend_old[k], pend_add[k]); // image += (float)total, engine.cpp:468
                     const double total_k = __dadd_rn(__dadd_rn(tot[k], pf[k]), pt[k]); // StepCache::total
                     const float add = __double2float_rn(total_k);
-                    if (add != 0.0f) {
-                        float* const p = rec + k * kSects + ((a.sect_packed[k] >> (3 * grp)) & 7u);
-                        *p = __fadd_rn(*p, add); // image += (float)total, engine.cpp:468
+                    float* const at_k = rec + k * kSects + ((a.sect_packed[k] >> (3 * grp)) & 7u);
+                    if (RED) {
+                        if (add != 0.0f) atomicAdd(at_k, add); // (result unused: a RED, nothing to wait for)
+                    } else {
+                        pend_at[k] = nullptr;
+                        if (add != 0.0f) {
+                            pend_at[k] = at_k;
+                            pend_old[k] = *at_k;
+                            pend_add[k] = add;
+                        }
                     }
                 }
             }
@@ -284,6 +303,11 @@ __global__ void __launch_bounds__(kThreads) k5_pairs_kernel(PairArgs a) {
         y0 = ny0;
 #pragma unroll
         for (int p = 0; p < PASSES; ++p) code[p] = next_code[p];
+    }
+    if (!RED) {
+#pragma unroll
+        for (int k = 0; k < kKinds; ++k)
+            if (pend_at[k]) *pend_at[k] = __fadd_rn(pend_old[k], pend_add[k]);
     }
 }
 
@@ -365,14 +389,24 @@ bool build_pair_tables(const WalkListsHost& w, int chunk_k, PairTables* out, std
 // Raises the kernel's dynamic shared-memory limit on the CURRENT device (the attribute is per
 // device) and sizes the persistent grid.
 template <int PASSES>
-cudaError_t prepare_one(size_t smem, int sm_count, int* ctas) {
-    cudaError_t e = cudaFuncSetAttribute(k5_pairs_kernel<PASSES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t prepare_one(size_t smem, int sm_count, int* ctas) { // ctas[0]: plain read-modify-write, ctas[1]: RED
+    cudaError_t e = cudaFuncSetAttribute(k5_pairs_kernel<PASSES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_pairs_kernel<PASSES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_pairs_kernel<PASSES>, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_pairs_kernel<PASSES, false>, kThreads, smem);
     if (e != cudaSuccess) return e;
-    *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+    ctas[0] = sm_count * (per_sm > 0 ? per_sm : 1);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_pairs_kernel<PASSES, true>, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    ctas[1] = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
+}
+
+template <int PASSES>
+void launch_one(cudaStream_t s, const PairArgs& a, bool red, unsigned blocks, size_t smem) {
+    if (red) k5_pairs_kernel<PASSES, true><<<blocks, kThreads, smem, s>>>(a);
+    else k5_pairs_kernel<PASSES, false><<<blocks, kThreads, smem, s>>>(a);
 }
 
 cudaError_t prepare_k5_pairs(const PairTables& t, int sm_count, int* ctas) {
@@ -410,18 +444,19 @@ cudaError_t launch_k5_pairs(cudaStream_t s, const K5Launch& l) {
     a.n_tiles = a.tiles_x * ((l.g.rows + kMarkTileH - 1) / kMarkTileH);
     a.inv_tiles_x = (uint32_t)std::min<unsigned long long>(0x100000000ull / (unsigned long long)a.tiles_x, 0xFFFFFFFFull);
     a.advance_tick = l.advance_tick;
-    long long blocks = l.pairs_ctas > 0 ? l.pairs_ctas : 148;
+    const bool red = l.pairs_red != 0;
+    long long blocks = l.pairs_ctas[red ? 1 : 0] > 0 ? l.pairs_ctas[red ? 1 : 0] : 148;
     if (a.marks.epoch == nullptr && blocks > a.n_tiles) blocks = a.n_tiles; // one CTA covers a tile per round
     if (blocks < 1) blocks = 1;
     const size_t smem = pairs_smem(t);
     switch (2 + t.hh) {
-        case 2: k5_pairs_kernel<2><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 3: k5_pairs_kernel<3><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 4: k5_pairs_kernel<4><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 5: k5_pairs_kernel<5><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 6: k5_pairs_kernel<6><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 7: k5_pairs_kernel<7><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
-        case 8: k5_pairs_kernel<8><<<(unsigned)blocks, kThreads, smem, s>>>(a); break;
+        case 2: launch_one<2>(s, a, red, (unsigned)blocks, smem); break;
+        case 3: launch_one<3>(s, a, red, (unsigned)blocks, smem); break;
+        case 4: launch_one<4>(s, a, red, (unsigned)blocks, smem); break;
+        case 5: launch_one<5>(s, a, red, (unsigned)blocks, smem); break;
+        case 6: launch_one<6>(s, a, red, (unsigned)blocks, smem); break;
+        case 7: launch_one<7>(s, a, red, (unsigned)blocks, smem); break;
+        case 8: launch_one<8>(s, a, red, (unsigned)blocks, smem); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -432,13 +432,19 @@ __global__ void dbg_vote_kernel(DebugArrays d, int fault) { // engine.cpp:365-38
     d.winners[su] = best_id;
 }
 
-__global__ void interleave_kernel(const float* __restrict__ plane, float* __restrict__ dyn, int kind, long long cells) {
+// Non-zero image values below this magnitude could produce subnormal sums (see Ctl::tiny_image).
+constexpr float kTinyImage = 2.0194839e-28f; // 2^-92
+
+__global__ void interleave_kernel(const float* __restrict__ plane, float* __restrict__ dyn, int kind, long long cells, Ctl* ctl) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; // one float4 (half a su record slot)
     if (t >= cells * 2) return;
     const long long cell = t >> 1;
     const int half = (int)(t & 1);
     const float4 v = reinterpret_cast<const float4*>(plane)[t];
     reinterpret_cast<float4*>(dyn)[cell * 6 + kind * 2 + half] = v;
+    const float lo = fminf(fminf(v.x != 0.f ? fabsf(v.x) : 1.f, v.y != 0.f ? fabsf(v.y) : 1.f),
+                           fminf(v.z != 0.f ? fabsf(v.z) : 1.f, v.w != 0.f ? fabsf(v.w) : 1.f));
+    if (lo < kTinyImage && ctl->tiny_image == 0) ctl->tiny_image = 1;
 }
 
 __global__ void deinterleave_kernel(const float* __restrict__ dyn, float* __restrict__ plane, int kind, long long cells) {
@@ -515,8 +521,8 @@ cudaError_t launch_dbg_vote(cudaStream_t s, const DebugArrays& d, int fault_inve
 }
 
 cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, int kind, long long cells_begin,
-                              long long cells) {
-    interleave_kernel<<<blocks_for(cells * 2, 256), 256, 0, s>>>(plane, dyn + cells_begin * (kKinds * kSects), kind, cells);
+                              long long cells, Ctl* ctl) {
+    interleave_kernel<<<blocks_for(cells * 2, 256), 256, 0, s>>>(plane, dyn + cells_begin * (kKinds * kSects), kind, cells, ctl);
     return cudaGetLastError();
 }
 

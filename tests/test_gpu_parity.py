@@ -173,6 +173,41 @@ def test_k5_active_tiles_and_window_kernel(product_lib, monkeypatch, name, path,
         assert_state_equal(gpu, cpu, f"{name} {path} knob {knob} tick {8 * (step + 1)}")
 
 
+@pytest.mark.parametrize("red", ["0", "1"])
+@pytest.mark.parametrize("name", ["desk64", "k2", "k4", "k16", "field-5x9", "closed-four", "wide-ragged", "sparse-periodic",
+                                  "d0.9-eight-ped1", "d0.5-bi-ped3"])
+def test_pair_kernel_image_update_variants(product_lib, monkeypatch, name, red):
+    """The pair kernel adds (float)total to the image either as a plain read-modify-write or as a
+    float reduction at the L2 (chosen when no image value can be subnormal — the reduction flushes
+    them); both forced here, both bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_PATH", "pairs")
+    monkeypatch.setenv("SFC_K5_RED", red)
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(4):
+        np.testing.assert_array_equal(gpu.run(8), cpu.run(8), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} red {red} tick {8 * (step + 1)}")
+
+
+def test_subnormal_image_values_stay_exact(product_lib):
+    """Uploaded images holding subnormal / tiny values: sums can be subnormal, which a float
+    reduction would flush — the engine must notice at upload and keep the exact path."""
+    text = sc.variant(sc.DESK64, rebuild_interval=0)
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    rng = np.random.default_rng(5)
+    for k in range(3):
+        img = cpu.image(k).copy()
+        tiny = rng.random(img.shape) < 0.3
+        img[tiny] = (rng.integers(1, 1 << 20, size=int(tiny.sum())).astype(np.uint32)).view(np.float32)  # subnormals
+        cpu.image(k)[:] = img  # (a view of the oracle's memory)
+        gpu.set_image(k, img)
+    for step in range(3):
+        np.testing.assert_array_equal(gpu.run(4), cpu.run(4))
+        assert_state_equal(gpu, cpu, f"subnormal tick {4 * (step + 1)}")
+
+
 def test_default_path_field13(product_lib):
     """13 x 13 fields in a crowd, no knobs: scatter kernel, crowded tiles handed to the list walk."""
     text = sc.EXTRA["field13-crowd"]
