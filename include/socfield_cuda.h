@@ -207,6 +207,21 @@ int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* m
  * halos with peer copies.  metrics: NULL or [ticks] (moved summed over slabs). */
 int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* metrics);
 
+/* ---- Validation without host copies.
+ * sfc_digest: the acceptance digest of the resident state — FNV-1a over occupancy, the three dynamic
+ * images, the centres — bit-identical to state_digest (tests/acceptance/acceptance_main.cpp:39-58),
+ * computed on the device (whole-grid engines only).
+ * sfc_compare: states_identical (engine.cpp:103-156) between the resident states of two whole-grid
+ * engines on the same device: the first difference in the reference's order. */
+typedef struct sfc_difference {
+    int32_t what;      /* 0 identical, 1 tick, 2 pedestrian count, 3 centre, 4 occupancy, 5 static image, 6 + k dynamic image k */
+    int64_t index;     /* pedestrian id / flat su index / flat image index (su * 8 + sect) */
+    int32_t ax, ay, bx, by; /* what == 3: the two centres; what == 4: ax, bx the two occupants */
+    float av, bv;      /* what >= 5: the two image values */
+} sfc_difference;
+int sfc_digest(sfc_engine* e, uint64_t* digest);
+int sfc_compare(sfc_engine* a, sfc_engine* b, sfc_difference* out);
+
 /* Counters for bench.py: kernels launched by this engine since creation, bytes copied. */
 typedef struct sfc_counters {
     int64_t kernel_launches;

@@ -140,7 +140,7 @@ def lib() -> C.CDLL:
         "so_decide": (C.c_int, [vp, i64, C.POINTER(i32), C.POINTER(dbl)]),
         "so_rebuild_images": (None, [vp, vp]),
         "so_set_static_fields": (C.c_int, [vp, i64, C.POINTER(SoAnchor)]),
-        "so_digest": (C.c_uint64, [vp]),
+        "so_digest": (C.c_uint64, [vp]), "so_set_threads": (None, [C.c_int]),
         "so_occupancy": (C.POINTER(i32), [vp]), "so_image": (C.POINTER(C.c_float), [vp, C.c_int]),
         "so_centers_x": (C.POINTER(i32), [vp]), "so_centers_y": (C.POINTER(i32), [vp]),
         "so_ped_attr": (C.POINTER(i32), [vp, C.c_int]),
@@ -277,6 +277,11 @@ class OracleSim:
 
     def digest(self) -> int:
         return int(self.L.so_digest(self.h))
+
+    @staticmethod
+    def set_threads(n: int) -> None:
+        """k-5 over n threads (static su partition, like the reference's parallel_for); results do not depend on n."""
+        lib().so_set_threads(int(n))
 
     # views (numpy arrays aliasing the oracle's memory)
     def _view(self, ptr, shape, dtype):

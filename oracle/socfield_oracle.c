@@ -12,6 +12,7 @@
 #include "socfield_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -834,9 +835,9 @@ static int64_t k4_move(so_sim* s) {
 }
 
 /* ref: engine.cpp:428-472 k5_writeback_range with accumulator.hpp:36-46 StepCache */
-static void k5_writeback(so_sim* s) {
+static void k5_range(so_sim* s, size_t su_begin, size_t su_end) {
     const int K = s->cfg.chunk_k;
-    for (size_t su = 0; su < (size_t)s->C; ++su) {
+    for (size_t su = su_begin; su < su_end; ++su) {
         const int tx = (int)(su % (size_t)s->W), ty = (int)(su / (size_t)s->W);
         for (int kind = 0; kind < SO_KINDS; ++kind) {
             const uint8_t* from_mask = s->from_mask[kind];
@@ -872,6 +873,45 @@ static void k5_writeback(so_sim* s) {
             }
         }
     }
+}
+
+/* The reference runs k-5 as a parallel_for over su with a static contiguous partition
+ * (engine.cpp:524-528, thread_pool.cpp:52-54): every su is written by exactly one worker and reads
+ * only the movement log, so the result does not depend on the worker count.  so_set_threads > 1 does
+ * the same here (large parity cases); the default is the plain loop. */
+static int g_threads = 1;
+void so_set_threads(int n) { g_threads = n < 1 ? 1 : (n > 64 ? 64 : n); }
+
+typedef struct {
+    so_sim* s;
+    size_t begin, end;
+} k5_job;
+
+static void* k5_worker(void* arg) {
+    k5_job* j = (k5_job*)arg;
+    k5_range(j->s, j->begin, j->end);
+    return NULL;
+}
+
+static void k5_writeback(so_sim* s) {
+    const size_t n = (size_t)s->C;
+    const int workers = g_threads;
+    if (workers <= 1 || n < 4096) {
+        k5_range(s, 0, n);
+        return;
+    }
+    pthread_t tid[64];
+    k5_job job[64];
+    int started = 0;
+    for (int w = 0; w < workers; ++w) { /* [n*w/workers, n*(w+1)/workers), thread_pool.cpp:52-54 */
+        job[w].s = s;
+        job[w].begin = n * (size_t)w / (size_t)workers;
+        job[w].end = n * (size_t)(w + 1) / (size_t)workers;
+        if (pthread_create(&tid[w], NULL, k5_worker, &job[w]) != 0) break;
+        ++started;
+    }
+    for (int w = started; w < workers; ++w) k5_range(s, job[w].begin, job[w].end);
+    for (int w = 0; w < started; ++w) pthread_join(tid[w], NULL);
 }
 
 /* ref: engine.cpp:538-550 maybe_rebuild + fields.cpp:144-150 max_abs_difference */

@@ -88,6 +88,7 @@ struct sfc_engine {
     PairTables pairs{};       // tables of the pair kernel (blob == nullptr: the field geometry does not fit it)
     int k5_pairs = 0;         // the pair kernel is the k-5 kernel (chosen in sfc_upload)
     int pairs_ctas[2] = {148, 148};
+    int listwalk_ctas = 148, window_ctas = 148; // persistent grids of the list-walk / window kernels for these tables
     int pairs_red = 0;        // its RED variant is exact for the uploaded state (sfc_upload)
     int pairs_red_tables = 0; // ... as far as the field magnitudes go (all >= 2^-40: sums are multiples of 2^-115)
     int pairs_red_pref = -1;  // SFC_K5_RED: 0 never, 1 always (tests), -1 when provably exact
@@ -374,6 +375,11 @@ int check_device_error(sfc_engine* e) {
         static const char* names[3] = {"dir-attractive", "dir-repulsive", "recurrent-repulsive"};
         std::snprintf(buf, sizeof buf, "%s image drifted by %s", names[std::clamp(h.error_x, 0, 2)],
                       std::to_string((float)h.error_value).c_str());
+    } else if (h.error_phase == 6) {
+        std::snprintf(buf, sizeof buf, "device error %d: halo exchange buffer overflow (%g records)", h.error_code, h.error_value);
+    } else if (h.error_phase == 4) {
+        std::snprintf(buf, sizeof buf, "device error %d in phase 4: event list of the slab overflowed (%g entries)", h.error_code,
+                      h.error_value);
     } else {
         std::snprintf(buf, sizeof buf, "device error %d in phase %d (rebuild list capacity exceeded: %g centres)",
                       h.error_code, h.error_phase, h.error_value);
@@ -407,6 +413,8 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.pairs_ctas[0] = e->pairs_ctas[0];
     l.pairs_ctas[1] = e->pairs_ctas[1];
     l.pairs_red = e->pairs_red;
+    l.listwalk_ctas = e->listwalk_ctas;
+    l.window_ctas = e->window_ctas;
     return l;
 }
 
@@ -652,10 +660,10 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(cudaMemset(e->dyn, 0, sizeof(float) * (size_t)e->cells * kKinds * kSects), "cudaMemset");
     cu(cudaMemset(e->ev, 0, (size_t)e->cells * 2), "cudaMemset");
     cu(prepare_k5_writeback(cfg->chunk_k, e->tabs), "cudaFuncSetAttribute(k5)");
-    cu(prepare_k5_listwalk(cfg->chunk_k, e->walk, e->sm_count), "cudaFuncSetAttribute(k5 list walk)");
+    cu(prepare_k5_listwalk(cfg->chunk_k, e->walk, e->sm_count, &e->listwalk_ctas), "cudaFuncSetAttribute(k5 list walk)");
     if (e->k5_tile_rows != kMarkTileH || !k5_listwalk_supported(e->walk)) e->k5_listwalk = 0; // (its tiles are 32 x 8)
     if (e->k5_window_ok)
-        cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count), "cudaFuncSetAttribute(k5 window)");
+        cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count, &e->window_ctas), "cudaFuncSetAttribute(k5 window)");
     if (e->k5_tile_rows != kMarkTileH) e->pairs.blob = nullptr;
     if (e->pairs.blob) cu(prepare_k5_pairs(e->pairs, e->sm_count, e->pairs_ctas), "cudaFuncSetAttribute(k5 pairs)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
@@ -774,6 +782,13 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         e->counters.h2d_bytes += (int64_t)((sizeof(int2) * 2 + sizeof(uint32_t)) * P);
     }
     if (e->slab.active) {
+        // k-4 lists the two event cells of every mover for the next tick's clear: any pedestrian may move
+        if (2 * P + 16 > e->slab.ev_capacity) {
+            cudaFree(e->slab.ev_written);
+            e->slab.ev_written = nullptr;
+            e->slab.ev_capacity = 2 * P + 16;
+            SFC_CUDA(dev_alloc(&e->slab.ev_written, e->slab.ev_capacity));
+        }
         e->ped_half_h = max_hh;
         e->slab.reach = max_hh + 1;
         const int need = 4 * (max_hh + 1) + (e->dp.regulated ? e->dp.density_radius : 0);
@@ -1306,6 +1321,76 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
         }
     }
     return status;
+}
+
+int sfc_digest(sfc_engine* e, uint64_t* digest) {
+    if (!e->uploaded) return fail(e, SFC_E_STATE, "digest before upload");
+    if (e->slab.active) return fail(e, SFC_E_STATE, "digest: whole-grid engines only");
+    SFC_CUDA(cudaSetDevice(e->device));
+    void* scratch = nullptr;
+    SFC_CUDA(cudaMalloc(&scratch, digest_scratch_bytes(e->cells, e->peds.n)));
+    unsigned long long* out = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) +
+                                                                    (digest_scratch_bytes(e->cells, e->peds.n) - 64));
+    cudaError_t c = launch_digest(e->stream, e->occ, e->dyn, e->peds.center, e->cells, e->peds.n, scratch, out);
+    unsigned long long h = 0;
+    if (c == cudaSuccess) c = cudaMemcpyAsync(&h, out, sizeof h, cudaMemcpyDeviceToHost, e->stream);
+    if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+    cudaFree(scratch);
+    if (c != cudaSuccess) return cuda_fail(e, c, "sfc_digest");
+    e->counters.kernel_launches += 2;
+    *digest = h;
+    return SFC_OK;
+}
+
+int sfc_compare(sfc_engine* a, sfc_engine* b, sfc_difference* out) {
+    sfc_engine* e = a;
+    if (!a->uploaded || !b->uploaded) return fail(e, SFC_E_STATE, "compare before upload");
+    if (a->slab.active || b->slab.active || a->device != b->device || a->g.W != b->g.W || a->g.H != b->g.H)
+        return fail(e, SFC_E_STATE, "compare: two whole-grid engines of one geometry on one device");
+    SFC_CUDA(cudaSetDevice(a->device));
+    *out = sfc_difference{};
+    int rc = check_device_error(a); // synchronises, refreshes the tick shadows
+    if (rc == SFC_OK) rc = check_device_error(b);
+    if (rc != SFC_OK && rc != SFC_E_INTEGRITY) return rc;
+    if (a->tick != b->tick) {
+        out->what = 1;
+        return SFC_OK;
+    }
+    if (a->peds.n != b->peds.n) {
+        out->what = 2;
+        return SFC_OK;
+    }
+    unsigned long long* first = nullptr;
+    SFC_CUDA(cudaMalloc(reinterpret_cast<void**>(&first), 6 * sizeof(unsigned long long)));
+    unsigned long long h[6];
+    cudaError_t c = launch_compare(a->stream, a->peds, b->peds, a->occ, b->occ, a->stat, b->stat, a->dyn, b->dyn, a->cells, first);
+    if (c == cudaSuccess) c = cudaMemcpyAsync(h, first, sizeof h, cudaMemcpyDeviceToHost, a->stream);
+    if (c == cudaSuccess) c = cudaStreamSynchronize(a->stream);
+    cudaFree(first);
+    if (c != cudaSuccess) return cuda_fail(e, c, "sfc_compare");
+    a->counters.kernel_launches += 1;
+    for (int w = 0; w < 6; ++w) { // the reference's order: centres, occupancy, static image, dynamic images
+        if (h[w] == ~0ull) continue;
+        out->what = 3 + w;
+        out->index = (int64_t)h[w];
+        if (w == 0) {
+            int2 ca, cb;
+            SFC_CUDA(cudaMemcpy(&ca, a->peds.center + h[w], sizeof ca, cudaMemcpyDeviceToHost));
+            SFC_CUDA(cudaMemcpy(&cb, b->peds.center + h[w], sizeof cb, cudaMemcpyDeviceToHost));
+            out->ax = ca.x, out->ay = ca.y, out->bx = cb.x, out->by = cb.y;
+        } else if (w == 1) {
+            SFC_CUDA(cudaMemcpy(&out->ax, a->occ + h[w], sizeof(int), cudaMemcpyDeviceToHost));
+            SFC_CUDA(cudaMemcpy(&out->bx, b->occ + h[w], sizeof(int), cudaMemcpyDeviceToHost));
+        } else {
+            const long long cell = (long long)(h[w] / kSects), sect = (long long)(h[w] % kSects);
+            const float* pa = w == 2 ? a->stat + h[w] : a->dyn + (cell * kKinds + (w - 3)) * kSects + sect;
+            const float* pb = w == 2 ? b->stat + h[w] : b->dyn + (cell * kKinds + (w - 3)) * kSects + sect;
+            SFC_CUDA(cudaMemcpy(&out->av, pa, sizeof(float), cudaMemcpyDeviceToHost));
+            SFC_CUDA(cudaMemcpy(&out->bv, pb, sizeof(float), cudaMemcpyDeviceToHost));
+        }
+        return SFC_OK;
+    }
+    return SFC_OK;
 }
 
 void sfc_get_counters(const sfc_engine* e, sfc_counters* out) {

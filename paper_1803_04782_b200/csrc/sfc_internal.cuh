@@ -224,6 +224,21 @@ struct PairTables {
     uint32_t sect_packed[kKinds]; // sect of kind k fed by sect group g in bits [3g, 3g + 3)
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is state of a (function, device) pair shared by every
+// engine of the process: raise it on the CURRENT device when an engine needs more, never lower it.
+struct SmemGrant {
+    size_t granted[64] = {};
+    cudaError_t raise(const void* fn, size_t want, size_t initial = 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+        if (granted[dev] < initial) granted[dev] = initial;
+        if (want <= granted[dev]) return cudaSuccess;
+        const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+        if (e == cudaSuccess) granted[dev] = want;
+        return e;
+    }
+};
+
 // ---- launchers (defined in the .cu files) --------------------------------------------------
 struct K5Launch {
     GridDev g;
@@ -247,6 +262,8 @@ struct K5Launch {
     PairTables pairs;    // k-5: tables of the pair kernel (blob == nullptr: field not supported)
     int pairs_path;      // k-5: the pair kernel is the k-5 kernel (every / every active tile)
     int pairs_ctas[2];   // k-5: its persistent grid ([1]: the RED variant)
+    int listwalk_ctas;   // k-5: persistent grid of the list-walk kernel for this engine's tables
+    int window_ctas;     // k-5: ... of the window kernel
     int pairs_red;       // k-5: image += (float)total as a float reduction at the L2 (no image value can be subnormal)
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
@@ -299,17 +316,23 @@ cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTab
 cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t);
 // window formulation of k-5 (sfc_k5_window.cu)
 bool k5_window_supported(const TablesDev& t);
-cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count);
+cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count, int* ctas);
 cudaError_t launch_k5_window(cudaStream_t s, const K5Launch& a);
 // list-walk formulation of k-5 (sfc_k5_listwalk.cu)
 bool build_walk_lists(const sfc_tables& t, WalkListsHost* out);
 bool k5_listwalk_supported(const WalkLists& w);
-cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count);
+cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count, int* ctas);
 cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& a, bool from_dense_list);
 // pair formulation of k-5 (sfc_k5_pairs.cu)
 bool build_pair_tables(const WalkListsHost& w, int chunk_k, PairTables* out, std::vector<unsigned char>* blob);
 cudaError_t prepare_k5_pairs(const PairTables& t, int sm_count, int* ctas);
 cudaError_t launch_k5_pairs(cudaStream_t s, const K5Launch& a);
 cudaError_t prepare_rebuild(const TablesDev& t);
+// acceptance digest / states_identical on the device (sfc_digest.cu)
+size_t digest_scratch_bytes(long long cells, long long peds);
+cudaError_t launch_digest(cudaStream_t s, const int* occ, const float* dyn, const int2* center, long long cells, long long peds,
+                          void* scratch, unsigned long long* out);
+cudaError_t launch_compare(cudaStream_t s, const PedArrays& pa, const PedArrays& pb, const int* oa, const int* ob, const float* sa,
+                           const float* sb, const float* da, const float* db, long long cells, unsigned long long* first);
 
 } // namespace sfc

@@ -256,29 +256,21 @@ LwShape lw_shape(const WalkLists& w) {
     return s;
 }
 
-struct LwPrepared {
-    size_t granted = 0;
-    int ctas = 0;
-};
-LwPrepared g_prepared[4];
-
 template <int K>
-cudaError_t prepare_one(const WalkLists& w, int sm_count, LwPrepared& st) {
+cudaError_t prepare_one(const WalkLists& w, int sm_count, int* ctas) {
+    static SmemGrant grant; // (one per kernel instantiation)
     const LwShape sh = lw_shape(w);
-    if (sh.smem > st.granted) {
-        const cudaError_t e = cudaFuncSetAttribute(k5_listwalk_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
-        if (e != cudaSuccess) return e;
-        st.granted = sh.smem;
-    }
-    int per_sm = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_listwalk_kernel<K, true>, kThreads, sh.smem);
+    cudaError_t e = grant.raise(reinterpret_cast<const void*>(k5_listwalk_kernel<K, true>), sh.smem);
     if (e != cudaSuccess) return e;
-    st.ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_listwalk_kernel<K, true>, kThreads, sh.smem);
+    if (e != cudaSuccess) return e;
+    *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
 }
 
 template <int K>
-cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_list, const LwPrepared& st) {
+cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_list) {
     const LwShape sh = lw_shape(l.walk);
     LwArgs a;
     a.g = l.g;
@@ -297,13 +289,11 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_l
     a.rh = sh.rh;
     a.list_smem = sh.list_smem;
     long long blocks = a.n_tiles;
-    if (blocks > st.ctas) blocks = st.ctas;
+    if (blocks > l.listwalk_ctas) blocks = l.listwalk_ctas;
     if (blocks < 1) blocks = 1;
     k5_listwalk_kernel<K, true><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a); // (supported lists always fit: kListSmemMax)
     return cudaGetLastError();
 }
-
-int k_index(int chunk_k) { return chunk_k == 2 ? 0 : (chunk_k == 4 ? 1 : (chunk_k == 8 ? 2 : 3)); }
 
 } // namespace
 
@@ -381,25 +371,23 @@ bool build_walk_lists(const sfc_tables& t, WalkListsHost* out) {
 // Fields up to 15 x 15 (the per-su cost grows with the field area whatever the crowd).
 bool k5_listwalk_supported(const WalkLists& w) { return w.meta != nullptr && w.n > 0 && w.n <= kListSmemMax; }
 
-cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count) {
+cudaError_t prepare_k5_listwalk(int chunk_k, const WalkLists& w, int sm_count, int* ctas) {
     if (!k5_listwalk_supported(w)) return cudaSuccess;
-    LwPrepared& st = g_prepared[k_index(chunk_k)];
     switch (chunk_k) {
-        case 2: return prepare_one<2>(w, sm_count, st);
-        case 4: return prepare_one<4>(w, sm_count, st);
-        case 8: return prepare_one<8>(w, sm_count, st);
-        case 16: return prepare_one<16>(w, sm_count, st);
+        case 2: return prepare_one<2>(w, sm_count, ctas);
+        case 4: return prepare_one<4>(w, sm_count, ctas);
+        case 8: return prepare_one<8>(w, sm_count, ctas);
+        case 16: return prepare_one<16>(w, sm_count, ctas);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& l, bool from_dense_list) {
-    const LwPrepared& st = g_prepared[k_index(l.chunk_k)];
     switch (l.chunk_k) {
-        case 2: return launch_one<2>(s, l, from_dense_list, st);
-        case 4: return launch_one<4>(s, l, from_dense_list, st);
-        case 8: return launch_one<8>(s, l, from_dense_list, st);
-        case 16: return launch_one<16>(s, l, from_dense_list, st);
+        case 2: return launch_one<2>(s, l, from_dense_list);
+        case 4: return launch_one<4>(s, l, from_dense_list);
+        case 8: return launch_one<8>(s, l, from_dense_list);
+        case 16: return launch_one<16>(s, l, from_dense_list);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -390,8 +390,9 @@ bool build_pair_tables(const WalkListsHost& w, int chunk_k, PairTables* out, std
 // device) and sizes the persistent grid.
 template <int PASSES>
 cudaError_t prepare_one(size_t smem, int sm_count, int* ctas) { // ctas[0]: plain read-modify-write, ctas[1]: RED
-    cudaError_t e = cudaFuncSetAttribute(k5_pairs_kernel<PASSES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_pairs_kernel<PASSES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static SmemGrant grant[2]; // (per kernel instantiation)
+    cudaError_t e = grant[0].raise(reinterpret_cast<const void*>(k5_pairs_kernel<PASSES, false>), smem);
+    if (e == cudaSuccess) e = grant[1].raise(reinterpret_cast<const void*>(k5_pairs_kernel<PASSES, true>), smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_pairs_kernel<PASSES, false>, kThreads, smem);

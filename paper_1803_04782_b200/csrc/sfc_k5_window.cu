@@ -424,37 +424,27 @@ __global__ void __launch_bounds__(kThreads, 3) k5_window_kernel(WinArgs a) {
     }
 }
 
-struct WinPrepared {
-    size_t granted[3] = {0, 0, 0}; // [tables in global, tables in shared memory, fast path]
-    int ctas = 0;
-};
-WinPrepared g_prepared[4];
-
 template <int K, bool TAB_SMEM, bool FAST>
-cudaError_t prepare_one(const WinShape& sh, int sm_count, WinPrepared& st) {
-    if (sh.smem > st.granted[TAB_SMEM + FAST]) {
-        const cudaError_t e = cudaFuncSetAttribute(k5_window_kernel<K, TAB_SMEM, FAST>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
-        if (e != cudaSuccess) return e;
-        st.granted[TAB_SMEM + FAST] = sh.smem;
-    }
-    int per_sm = 0;
-    const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_window_kernel<K, TAB_SMEM, FAST>, kThreads, sh.smem);
+cudaError_t prepare_one(const WinShape& sh, int sm_count, int* ctas) {
+    static SmemGrant grant; // (one per kernel instantiation)
+    cudaError_t e = grant.raise(reinterpret_cast<const void*>(k5_window_kernel<K, TAB_SMEM, FAST>), sh.smem);
     if (e != cudaSuccess) return e;
-    st.ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_window_kernel<K, TAB_SMEM, FAST>, kThreads, sh.smem);
+    if (e != cudaSuccess) return e;
+    *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
 }
 
 template <int K>
-cudaError_t prepare_k(const TablesDev& t, int /*ev_max*/, int sm_count, WinPrepared& st) {
+cudaError_t prepare_k(const TablesDev& t, int /*ev_max*/, int sm_count, int* ctas) {
     const WinShape sh = win_shape(t);
-    if (sh.tab_smem && same_box(t)) return prepare_one<K, true, true>(sh, sm_count, st);
-    return sh.tab_smem ? prepare_one<K, true, false>(sh, sm_count, st) : prepare_one<K, false, false>(sh, sm_count, st);
+    if (sh.tab_smem && same_box(t)) return prepare_one<K, true, true>(sh, sm_count, ctas);
+    return sh.tab_smem ? prepare_one<K, true, false>(sh, sm_count, ctas) : prepare_one<K, false, false>(sh, sm_count, ctas);
 }
 
 template <int K>
-cudaError_t launch_k(cudaStream_t stream, const K5Launch& l, const WinPrepared& st) {
+cudaError_t launch_k(cudaStream_t stream, const K5Launch& l) {
     const WinShape sh = win_shape(l.t);
     WinArgs a;
     a.g = l.g;
@@ -474,7 +464,7 @@ cudaError_t launch_k(cudaStream_t stream, const K5Launch& l, const WinPrepared& 
     a.table_bytes = sh.table_bytes;
     static const int knob = std::getenv("SFC_K5_WINDOW_CTAS") ? std::atoi(std::getenv("SFC_K5_WINDOW_CTAS")) : 0;
     long long blocks = (long long)l.marks.tiles_x * l.marks.tiles_y * kBlocksPerTile / kWarps + 1;
-    const int cap = knob > 0 ? knob : st.ctas;
+    const int cap = knob > 0 ? knob : (l.window_ctas > 0 ? l.window_ctas : 148);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     if (sh.tab_smem && same_box(l.t))
@@ -486,8 +476,6 @@ cudaError_t launch_k(cudaStream_t stream, const K5Launch& l, const WinPrepared& 
     return cudaGetLastError();
 }
 
-int k_index(int chunk_k) { return chunk_k == 2 ? 0 : (chunk_k == 4 ? 1 : (chunk_k == 8 ? 2 : 3)); }
-
 } // namespace
 
 // The window kernel keeps one 64-bit word per region column (4 + 2*hh rows) and packs region
@@ -497,25 +485,23 @@ bool k5_window_supported(const TablesDev& t) {
     return win_shape(t).smem <= 220 * 1024;
 }
 
-cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count) {
+cudaError_t prepare_k5_window(int chunk_k, const TablesDev& t, int ev_max, int sm_count, int* ctas) {
     if (!k5_window_supported(t)) return cudaSuccess;
-    WinPrepared& st = g_prepared[k_index(chunk_k)];
     switch (chunk_k) {
-        case 2: return prepare_k<2>(t, ev_max, sm_count, st);
-        case 4: return prepare_k<4>(t, ev_max, sm_count, st);
-        case 8: return prepare_k<8>(t, ev_max, sm_count, st);
-        case 16: return prepare_k<16>(t, ev_max, sm_count, st);
+        case 2: return prepare_k<2>(t, ev_max, sm_count, ctas);
+        case 4: return prepare_k<4>(t, ev_max, sm_count, ctas);
+        case 8: return prepare_k<8>(t, ev_max, sm_count, ctas);
+        case 16: return prepare_k<16>(t, ev_max, sm_count, ctas);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_k5_window(cudaStream_t s, const K5Launch& l) {
-    const WinPrepared& st = g_prepared[k_index(l.chunk_k)];
     switch (l.chunk_k) {
-        case 2: return launch_k<2>(s, l, st);
-        case 4: return launch_k<4>(s, l, st);
-        case 8: return launch_k<8>(s, l, st);
-        case 16: return launch_k<16>(s, l, st);
+        case 2: return launch_k<2>(s, l);
+        case 4: return launch_k<4>(s, l);
+        case 8: return launch_k<8>(s, l);
+        case 16: return launch_k<16>(s, l);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -719,16 +719,11 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l) {
     return cudaGetLastError();
 }
 
-// The attribute is per-function process state shared by every engine: only ever raise it.
 template <int K, int SG, int ROWS, int NT, int MODE>
 cudaError_t prepare_one(const TablesDev& t) {
-    static size_t granted = 0;
-    const size_t want = k5_shape<K, SG, ROWS, NT, MODE>(t).smem;
-    if (want <= granted) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(k5_writeback_kernel<K, SG, ROWS, NT, MODE>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
-    if (e == cudaSuccess) granted = want;
-    return e;
+    static SmemGrant grant; // (one per kernel instantiation)
+    return grant.raise(reinterpret_cast<const void*>(k5_writeback_kernel<K, SG, ROWS, NT, MODE>),
+                       k5_shape<K, SG, ROWS, NT, MODE>(t).smem);
 }
 
 // Small fields (the whole 32 x 8 tile region is staged at once, tables in shared memory): scatter

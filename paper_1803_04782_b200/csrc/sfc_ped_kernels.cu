@@ -353,6 +353,8 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
                 if (at + 1 < slab.ev_capacity) {
                     slab.ev_written[at] = from >= 0 ? 2 * from : -1;
                     slab.ev_written[at + 1] = to >= 0 ? 2 * to + 1 : -1;
+                } else { // (sized for two entries per resident pedestrian at upload: cannot happen)
+                    raise_error(ctl, SFC_E_STATE, 4, nx, ny, (double)at);
                 }
             }
             if (dbg.moved_from) { // MovementLog as the reference shapes it (engine.cpp:412-423)

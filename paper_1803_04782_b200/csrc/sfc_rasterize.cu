@@ -233,12 +233,8 @@ size_t rebuild_smem(const TablesDev& t) {
 
 // Raises the dynamic shared-memory limit ahead of time (must not happen inside a graph capture).
 cudaError_t prepare_rebuild(const TablesDev& t) {
-    static size_t granted = 48 * 1024; // per-function process state shared by every engine: only raise it
-    const size_t smem = rebuild_smem(t);
-    if (smem <= granted) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(rebuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) granted = smem;
-    return e;
+    static SmemGrant grant;
+    return grant.raise(reinterpret_cast<const void*>(rebuild_kernel), rebuild_smem(t), 48 * 1024);
 }
 
 cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,

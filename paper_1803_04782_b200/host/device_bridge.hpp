@@ -74,4 +74,8 @@ private:
 sfc_engine* create_engine(const GridGeometry& g, const EngineConfig& cfg,
                           const std::array<KindTable, kDynKinds>& tables);
 
+
+// rasterize_static(fields) into the static image of a live engine, on its device (no host image).
+void rasterize_static_on(sfc_engine* h, const std::vector<AnchoredField>& fields);
+
 } // namespace socfield::bridge

@@ -393,6 +393,38 @@ std::vector<SuIndex> Engine::download_centers() {
     return out;
 }
 
+void Engine::set_static_resident(const std::vector<AnchoredField>& fields) {
+    bridge::rasterize_static_on(dev_, fields);
+}
+
+std::uint64_t Engine::digest_resident() {
+    std::uint64_t h = 0;
+    const int status = sfc_digest(dev_, &h);
+    if (status != SFC_OK) throw_status(status);
+    return h;
+}
+
+bool Engine::resident_identical(Engine& other, std::string* diagnosis) { // wording of states_identical, engine.cpp:103-156
+    sfc_difference d{};
+    const int status = sfc_compare(dev_, other.dev_, &d);
+    if (status != SFC_OK) throw_status(status);
+    if (d.what == 0) return true;
+    std::ostringstream os;
+    const long w = geom_.width;
+    if (d.what == 1) os << "tick counter differs";
+    else if (d.what == 2) os << "pedestrian count differs";
+    else if (d.what == 3)
+        os << "pedestrian " << d.index << " center (" << d.ax << "," << d.ay << ") vs (" << d.bx << "," << d.by << ")";
+    else if (d.what == 4) os << "occupancy at su (" << d.index % w << "," << d.index / w << "): " << d.ax << " vs " << d.bx;
+    else {
+        const char* name = d.what == 5 ? "static" : field_kind_name(to_field_kind(static_cast<DynKind>(d.what - 6)));
+        os << name << " image at su (" << (d.index / kSects) % w << "," << (d.index / kSects) / w << ") sect " << d.index % kSects
+           << ": " << d.av << " vs " << d.bv;
+    }
+    if (diagnosis) *diagnosis = os.str();
+    return false;
+}
+
 std::vector<TickMetrics> Engine::step_resident(long ticks, bool phase_times) {
     std::vector<TickMetrics> out;
     if (ticks <= 0) return out;

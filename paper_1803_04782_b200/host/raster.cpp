@@ -30,10 +30,9 @@ struct DeviceHandle {
     ~DeviceHandle() { sfc_destroy(h); }
 };
 
-// Adds `items` (spec, centre) in list order to `base` (or to zeros) on the device.
-StrengthImage rasterize_list(const GridGeometry& g, const std::vector<AnchoredField>& items, const StrengthImage* base) {
-    DeviceHandle dev;
-    dev.h = bridge::create_engine(g, EngineConfig{}, unit_tables());
+// Adds `items` (spec, centre) in list order to `base` (or to zeros) in the static image of engine `h`;
+// copies the result to `out` when that is not null.
+void rasterize_on(sfc_engine* h, const std::vector<AnchoredField>& items, const float* base, float* out) {
     std::map<SpecKey, int> table_of;
     std::vector<bridge::KindTable> storage;
     std::vector<sfc_anchor> anchors;
@@ -46,15 +45,24 @@ StrengthImage rasterize_list(const GridGeometry& g, const std::vector<AnchoredFi
     }
     std::vector<sfc_kind_table> views;
     for (const auto& t : storage) views.push_back(t.view());
+    const int status = sfc_rasterize_static(h, static_cast<std::int32_t>(views.size()), views.data(),
+                                            static_cast<std::int64_t>(anchors.size()), anchors.data(), base, out);
+    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(h), -1, 0);
+}
+
+StrengthImage rasterize_list(const GridGeometry& g, const std::vector<AnchoredField>& items, const StrengthImage* base) {
+    DeviceHandle dev;
+    dev.h = bridge::create_engine(g, EngineConfig{}, unit_tables());
     StrengthImage out(g);
-    const int status = sfc_rasterize_static(dev.h, static_cast<std::int32_t>(views.size()), views.data(),
-                                            static_cast<std::int64_t>(anchors.size()), anchors.data(),
-                                            base ? base->raw().data() : nullptr, out.raw_mut().data());
-    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(dev.h), -1, 0);
+    rasterize_on(dev.h, items, base ? base->raw().data() : nullptr, out.raw_mut().data());
     return out;
 }
 
 } // namespace
+
+void bridge::rasterize_static_on(sfc_engine* h, const std::vector<AnchoredField>& fields) {
+    rasterize_on(h, fields, nullptr, nullptr);
+}
 
 StrengthImage rasterize_static(const std::vector<AnchoredField>& fields, const GridGeometry& g) {
     return rasterize_list(g, fields, nullptr);

@@ -81,3 +81,45 @@ EXTRA = {
                      "rebuild_interval = 6\n",
     "wide-ragged": "grid = 131x67\ndensity = 0.3\ndirections = bi\nwalk_period = 1..3\nseed = 123\nrebuild_interval = 10\n",
 }
+
+
+# ---- BASELINE.json configs at (or shaped like) their stated parameters ------------------------
+# c1 and c2 are the configs themselves over their full / a long horizon; c3, c4 and c5 keep the
+# config's density, field geometry, regulation and obstacle share on a grid the CPU reference can
+# hold and finish (SURVEY.md 8c "scale limits").  Reference-recorded digests of each live in
+# tests/golden/baseline_shaped.json (tests/golden/make_golden.py --big).
+C1_TEXT = ("grid = 200x200\nboundary = closed\ndensity = 0.0125\ndirections = uni\nfield_geometry = 7x7\n"
+           "seed = 42\nrebuild_interval = 50\n")
+C1_EXIT = [(0, 399, 399, 1.0, -0.02, 199, 100)]  # one omni-attractive field anchored at the exit su, reaching the whole room
+C2_TEXT = ("grid = 2000x500\nboundary = periodic\ndensity = 0.02\ndirections = bi\nwalk_period = 1..3\n"
+           "field_geometry = 7x7\nseed = 42\nrebuild_interval = 50\n")
+
+
+def obstacle_anchors(width, height, share=0.01, seed=7):
+    """7 x 7 omni-repulsive static fields on `share` of the su; positions from a seeded 64-bit LCG
+    (self-contained: no dependence on a numpy bit-generator's stream)."""
+    n = int(round(share * width * height))
+    seen, out, x = set(), [], seed
+    while len(out) < n:
+        x = (x * 6364136223846793005 + 1442695040888963407) % (1 << 64)
+        at = (x >> 33) % (width * height)
+        if at in seen:
+            continue
+        seen.add(at)
+        out.append((1, 7, 7, 1.0, -0.5, at % width, at // width))
+    return out
+
+
+BASELINE_SHAPED = {
+    "c1-full": dict(text=C1_TEXT, static=C1_EXIT, ticks=[100, 500, 1000]),
+    "c2-100": dict(text=C2_TEXT, static=[], ticks=[1, 10, 50, 100]),
+    # c3: 35 x 35 fields (1224 support offsets) at rho 200000 / 2^26, two rebuilds inside the horizon
+    "c3-1024": dict(text="grid = 1024x1024\ndensity = 0.00298023223876953125\ndirections = eight\nfield_geometry = 35x35\n"
+                         "seed = 42\nrebuild_interval = 2\n", static=[], ticks=[2, 4]),
+    # c4: 7 x 7 fields at rho 10^6 / 2^30 (one mover per ~1000 su: active-tile list), two rebuilds
+    "c4-4096": dict(text="grid = 4096x4096\ndensity = 0.000931322574615478515625\ndirections = eight\nfield_geometry = 7x7\n"
+                         "seed = 42\nrebuild_interval = 6\n", static=[], ticks=[6, 12]),
+    # c5: 77 x 77 fields (5928 offsets) WITH linear regulation r = 3 and 7 x 7 obstacle fields on 1 % of the su, rho 0.05
+    "c5-256": dict(text="grid = 256x192\ndensity = 0.05\ndirections = eight\nfield_geometry = 77x77\nregulation = linear\n"
+                        "density_radius = 3\nseed = 42\nrebuild_interval = 4\n", static=obstacle_anchors(256, 192), ticks=[3, 6]),
+}

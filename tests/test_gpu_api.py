@@ -91,6 +91,25 @@ def test_resident_stepping_equals_run():
     assert e.counters()["kernel_launches"] > 0
 
 
+def test_one_engine_on_states_of_different_population():
+    """Engine::run(SimState&, ...) takes any state of the engine's grid (engine.hpp:157-160).  A
+    larger population, then a smaller one that fits the device arrays of the first, then the larger
+    again: the replayed tick graph must follow the population size."""
+    base = "grid = 48x40\ndirections = eight\nwalk_period = 1..2\nrebuild_interval = 6\n"
+    texts = [base + "density = 0.5\nseed = 11\n", base + "density = 0.2\nseed = 12\n", base + "density = 0.45\nseed = 13\n"]
+    engine = sf.Engine(sf.parse_scenario(texts[0]))
+    for text in texts:
+        state = sf.seed_population(sf.parse_scenario(text))
+        cpu = oracle.OracleSim.from_scenario(text)
+        for _ in range(2):
+            moved = [m.moved for m in engine.run(state, 9)]
+            np.testing.assert_array_equal(moved, cpu.run(9))
+            np.testing.assert_array_equal(state.centers(), cpu.centers())
+            np.testing.assert_array_equal(state.occupancy(), cpu.occupancy())
+            for k, kind in enumerate(("dir-attractive", "dir-repulsive", "recurrent-repulsive")):
+                np.testing.assert_array_equal(bits(state.image(kind)), bits(cpu.image(k)))
+
+
 # ---- reference tests/unit/test_engine.cpp ---------------------------------------------------
 
 def test_empty_grid_only_advances_the_counter(product_lib):

@@ -29,6 +29,45 @@ def test_oracle_reproduces_golden_digest(name):
         assert f"{sim.digest():#018x}" == digest, f"{name} at tick {tick}"
 
 
+BIG = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "baseline_shaped.json")))
+
+
+@pytest.mark.parametrize("name", sorted(BIG))
+def test_oracle_reproduces_baseline_shaped_digests(name):
+    """BASELINE configs 1-5 at / shaped like their stated parameters (tests/scenarios.py
+    BASELINE_SHAPED): c1 over 1000 ticks, c2 over 100, 35 x 35 fields, the c4 crowd on 4096^2,
+    77 x 77 fields with linear regulation and obstacle fields — digests recorded from the unmodified
+    reference.  The oracle's k-5 runs on every core here (static su partition, like the reference's
+    parallel_for: the result does not depend on the worker count)."""
+    g = BIG[name]
+    oracle.OracleSim.set_threads(os.cpu_count() or 1)
+    try:
+        sim = oracle.OracleSim.from_scenario(g["scenario"])
+        if g["static_fields"]:
+            sim.set_static_fields([tuple(a) for a in g["static_fields"]])
+        assert sim.population == g["population"]
+        last = 0
+        for tick, digest in g["digests"]:
+            sim.run(tick - last)
+            last = tick
+            assert f"{sim.digest():#018x}" == digest, f"{name} at tick {tick}"
+    finally:
+        oracle.OracleSim.set_threads(1)
+
+
+def test_oracle_k5_does_not_depend_on_the_thread_count():
+    text = "grid = 96x80\ndensity = 0.3\ndirections = eight\nwalk_period = 1..2\nseed = 6\nrebuild_interval = 5\n"
+    a = oracle.OracleSim.from_scenario(text)
+    b = oracle.OracleSim.from_scenario(text)
+    a.run(12)
+    oracle.OracleSim.set_threads(5)
+    try:
+        b.run(12)
+    finally:
+        oracle.OracleSim.set_threads(1)
+    assert a.digest() == b.digest()
+
+
 def test_survey_vectors_are_in_the_fixture():
     """The five digests quoted in SURVEY.md 8(c) (captured independently of this repo)."""
     desk = dict(GOLDEN["desk64"]["digests"])
