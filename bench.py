@@ -83,9 +83,6 @@ WORKLOADS = {
 }
 
 BYTES_PER_SU_K5 = 194.0       # 3 images x 32 B read + written, 2 B event-map read
-# dram__bytes_read.sum + dram__bytes_write.sum of one k-5 launch (the list-walk kernel) at config 2, from the
-# committed ncu --set full capture (profiles/r1c_k5_listwalk_c2.metrics.txt); not re-measured by the bench run
-K5_DRAM_TRAFFIC_C2 = 53.064192e6 + 5.001728e6
 BYTES_PER_SU_TICK = 200.0     # B_su
 BYTES_PER_PED_TICK = 200.0    # B_ped
 
@@ -96,6 +93,38 @@ def measured_peaks():
         with open(path) as f:
             return json.load(f).get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def k5_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the k-5 kernels of one tick, from the committed ncu
+    capture of this workload (profiles/r2_traffic.json, written by profiles/traffic.py on a B200), or None."""
+    path = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        rec = json.load(f).get(workload)
+    if not rec:
+        return None, None
+    return rec["dram_read_bytes_per_k5_phase"] + rec["dram_write_bytes_per_k5_phase"], rec.get("source")
+
+
+def k5_roofline(workload: str, cells: int, k5_us: float, kernel: str):
+    """The contract's roofline object for the k-5 phase: algorithmic bytes (194 B per su, every su) over its
+    CUDA-event duration against the measured HBM peak — plus, because k-5 only touches su within reach
+    of a mover, the same with the DRAM bytes it actually moved (`touched_frac`: the figure to read for
+    sparse crowds, where the algorithmic fraction exceeds 1)."""
+    peak, peak_src = measured_peaks()
+    achieved = BYTES_PER_SU_K5 * cells / (k5_us * 1e-6) / 1e9 if k5_us > 0 else None
+    traffic, src = k5_traffic(workload)
+    touched = traffic / (k5_us * 1e-6) / 1e9 if traffic and k5_us > 0 else None
+    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": src,
+            "touched_gbs": touched, "touched_frac": (touched / peak) if touched else None,
+            "peak_source": peak_src, "bytes_per_launch": BYTES_PER_SU_K5 * cells, "k5_us": k5_us}
+
+
+K5_KERNEL = {"pairs": "k5_pairs_kernel (one launch per tick)", "listwalk": "k5_listwalk_kernel",
+             "window": "k5_window_kernel + dense hand-off", "scatter+gather": "k5_writeback_kernel (scatter / event-walk gather)"}
 
 
 class ClockSampler(threading.Thread):
@@ -185,17 +214,103 @@ def barrier(dist, local: int):
 def build_state(sf, w):
     cfg = sf.parse_scenario(w["text"])
     state = sf.seed_population(cfg)
-    if "exit" in w:  # c1: one omni-attractive field anchored at the exit, reaching the whole room
-        state.set_static_fields([(sf.FieldSpec("omni-attractive", (399, 399), 1.0, -0.02), w["exit"])])
-    if "obstacles" in w:  # c5: dense obstacles = 7x7 omni-repulsive static fields on a seeded share of the su (seed 7)
+    fields = static_fields_of(sf, w, cfg)
+    if fields:
+        state.set_static_fields(fields)
+    return cfg, state
+
+
+def static_fields_of(sf, w, cfg):
+    """[(FieldSpec, (x, y)), ...] of a workload's static image: c1's exit, c5's obstacle fields."""
+    if "exit" in w:  # one omni-attractive field anchored at the exit, reaching the whole room
+        return [(sf.FieldSpec("omni-attractive", (399, 399), 1.0, -0.02), w["exit"])]
+    if "obstacles" in w:  # 7x7 omni-repulsive static fields on a seeded share of the su (seed 7)
         import numpy as np
 
         gw, gh = cfg.grid.width, cfg.grid.height
         n = int(round(w["obstacles"] * gw * gh))
         at = np.random.Generator(np.random.MT19937(7)).choice(gw * gh, size=n, replace=False)
         spec = sf.FieldSpec("omni-repulsive", (7, 7), 1.0, -0.5)
-        state.set_static_fields([(spec, (int(a % gw), int(a // gw))) for a in at])
-    return cfg, state
+        return [(spec, (int(a % gw), int(a // gw))) for a in at]
+    return []
+
+
+def make_resident(sf, w, device: int):
+    """An engine with the workload's seeded state resident in HBM, built WITHOUT a host SimState:
+    population seeded on the device (Engine.seed_resident), static fields rasterised on the device."""
+    cfg = sf.parse_scenario(w["text"])
+    engine = sf.Engine(cfg, 0, device)
+    P = engine.seed_resident(cfg)
+    fields = static_fields_of(sf, w, cfg)
+    if fields:
+        engine.set_static_fields(fields)
+    return engine, P
+
+
+def measure_resident(engine, P: int, cells: int, ticks_per_step: int, steps: int, warmup: int):
+    """(pedestrian-steps/s, tick_us, k5_us, phase_us[5]) of an HBM-resident run: `warmup` untimed steps,
+    `steps` timed steps (CUDA events on the engine's stream), then one step with per-phase events."""
+    for _ in range(warmup):
+        engine.step_resident(ticks_per_step)
+    total_ms = 0.0
+    for _ in range(steps):
+        engine.step_resident(ticks_per_step)
+        total_ms += engine.counters()["last_run_ms"]
+    ticks = ticks_per_step * steps
+    phase = engine.step_resident(ticks_per_step, True)
+    phase_us = [sum(m.phase_us[p] for m in phase) / len(phase) for p in range(5)]
+    plain = [m for m in phase if (m.tick + 1) % 50 != 0] or phase  # ticks whose k-5 slot holds no rebuild
+    k5_us = sum(m.phase_us[4] for m in plain) / len(plain)
+    return P * ticks / (total_ms * 1e-3), total_ms * 1e3 / ticks, k5_us, phase_us
+
+
+def other_configs(sf, device: int, skip: str):
+    """The other BASELINE configs on this GPU (HBM-resident, seeded on the device), a few steps each:
+    the `configs` block of the JSON line.  c4 is the full 32768^2 grid (144 GB resident)."""
+    out = {}
+    for name, steps in (("c1", 3), ("c3", 2), ("c4", 2), ("c5", 2)):
+        if name == skip:
+            continue
+        w = WORKLOADS[name]
+        try:
+            engine, P = make_resident(sf, w, device)
+            tps = w.get("ticks_per_step", TICKS_PER_STEP)
+            value, tick_us, k5_us, phase_us = measure_resident(engine, P, w["cells"], tps, steps, 3 if name != "c5" else 1)
+            c = engine.counters()
+            out[name] = {"workload": w["label"], "value": value, "unit": "pedestrian-steps/s",
+                         "su_updates_per_s": value * w["cells"] / P, "tick_us": tick_us, "ticks_timed": tps * steps,
+                         "k5_path": c.get("k5_path"), "k5_active_list": c.get("k5_active_list"),
+                         "phase_us_per_tick": {f"k{i + 1}": phase_us[i] for i in range(5)},
+                         "roofline": k5_roofline(name, w["cells"], k5_us, K5_KERNEL.get(c.get("k5_path"), "k-5"))}
+            del engine
+        except Exception as exc:  # a config that does not fit this GPU must not take the headline down
+            out[name] = {"workload": w["label"], "error": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+def parity_check(sf, device: int):
+    """Full-horizon divergence report against digests recorded from the UNMODIFIED reference
+    (tests/golden/baseline_shaped.json): c2 over 100 ticks, c1 over its 1000, digest of the resident
+    state computed on the device.  Decisions and positions are required to be bit-exact and the
+    field images are too, so the first divergent tick is either None or a bug."""
+    path = os.path.join(ROOT, "tests", "golden", "baseline_shaped.json")
+    if not os.path.exists(path):
+        return None
+    golden = json.load(open(path))
+    out = {"oracle": "FNV-1a state digests recorded from the unmodified reference (tests/golden/make_golden.py --big)",
+           "compared": "occupancy, the three dynamic images, centres — bit for bit (device-side digest, sfc_digest)"}
+    for name, key in (("c2", "c2-100"), ("c1", "c1-full")):
+        engine, P = make_resident(sf, WORKLOADS[name], device)
+        first, last, checked = None, 0, []
+        for tick, digest in golden[key]["digests"]:
+            engine.step_resident(tick - last)
+            last = tick
+            checked.append(tick)
+            if first is None and f"{engine.digest():#018x}" != digest:
+                first = tick
+        out[name] = {"checked_ticks": checked, "horizon": last, "first_divergent_tick": first}
+        del engine
+    return out
 
 
 def cpu_reference(w, ticks_per_step: int, steps: int, warmup: int):
@@ -303,6 +418,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the `configs` block (the other BASELINE configs) and the parity report")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: run the N > 1 slab path with every rank on GPU 0 (single-GPU smoke test of that path)")
     args = ap.parse_args()
@@ -381,7 +497,6 @@ def main():
     plain = [m for m in phase if (m.tick + 1) % 50 != 0] or phase  # ticks whose k-5 slot holds no rebuild
     k5_us = sum(m.phase_us[4] for m in plain) / len(plain)
     peak, peak_src = measured_peaks()
-    achieved = BYTES_PER_SU_K5 * C / (k5_us * 1e-6) / 1e9 if k5_us > 0 else None
     tick_us = total_ms * 1e3 / ticks
     tick_gbs = (BYTES_PER_SU_TICK * C + BYTES_PER_PED_TICK * P) / (tick_us * 1e-6) / 1e9
 
@@ -410,8 +525,10 @@ def main():
         return 0
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        # ~10 s of host work at config 2 (0.15 s per tick on 16 cores); the large configs take minutes per tick
-        r = cpu_reference(w, REF_TICKS_PER_STEP, 32 if args.workload in ("c1", "c2") else 1, 1 if args.workload in ("c1", "c2") else 0)
+        # the same sample as the reference arm (`--impl reference` with the same --steps / --warmup): ~6 s of host
+        # work at config 2 (0.15 s per tick on 16 cores); the large configs take minutes per tick
+        small = args.workload in ("c1", "c2")
+        r = cpu_reference(w, REF_TICKS_PER_STEP, args.steps if small else 1, args.warmup if small else 0)
         cpu = {"value": r["value"], "unit": "pedestrian-steps/s", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
     line = {
         "metric": "pedestrian-steps/s", "value": value, "unit": "pedestrian-steps/s",
@@ -434,15 +551,14 @@ def main():
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
-        "roofline": {"bound": "hbm", "kernel": "k-5 write-back, all k-5 kernels of a tick (k5_listwalk_kernel alone at configs 1, 2 and the paper baseline; "
-                               "k5_window_kernel + dense hand-off at config 4; k5_writeback_kernel gather at configs 3, 5)",
-                     "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                     "traffic": K5_DRAM_TRAFFIC_C2 if args.workload == "c2" else None,
-                     "peak_source": peak_src, "bytes_per_launch": BYTES_PER_SU_K5 * C,
-                     "whole_tick_gbs": tick_gbs, "whole_tick_frac": tick_gbs / peak},
+        "roofline": dict(k5_roofline(args.workload, C, k5_us, K5_KERNEL.get(c1.get("k5_path"), "k-5")),
+                         whole_tick_gbs=tick_gbs, whole_tick_frac=tick_gbs / peak),
         "cpu_baseline": cpu,
     }
+    if not args.no_configs and world == 1:
+        del engine
+        line["configs"] = other_configs(sf, local, args.workload)
+        line["parity"] = parity_check(sf, local)
     print(json.dumps(line))
     return 0
 

@@ -1,8 +1,12 @@
 """Short device-resident run for ncu: seeds a bench workload, uploads it, steps a few ticks.
 
-    ncu ... python profiles/profile_target.py --workload c2 --ticks 8
+    ncu --profile-from-start off ... python profiles/profile_target.py --workload c2 --ticks 8
+
+Only the last `--ticks` ticks (plain launches, one kernel per phase) lie between cuProfilerStart /
+cuProfilerStop; without `--profile-from-start off` ncu also sees the warm-up ticks (graph launches).
 """
 import argparse
+import ctypes
 import os
 import sys
 
@@ -17,11 +21,13 @@ ap.add_argument("--workload", default="c2")
 ap.add_argument("--ticks", type=int, default=8)
 ap.add_argument("--warm", type=int, default=30)
 args = ap.parse_args()
-cfg, state = bench.build_state(sf, bench.WORKLOADS[args.workload])
-engine = sf.Engine(cfg)
-engine.upload(state)
+w = bench.WORKLOADS[args.workload]
+engine, P = bench.make_resident(sf, w, 0)
 engine.step_resident(args.warm)      # let the crowd start moving (graph launches)
+cu = ctypes.CDLL("libcuda.so.1")
+cu.cuProfilerStart()
 m = engine.step_resident(args.ticks, True)  # plain launches, one kernel per phase
+cu.cuProfilerStop()
 print("moved per tick:", [x.moved for x in m])
 k5 = [x.phase_us[4] for x in m]
 print("k5 us per tick: avg %.1f min %.1f" % (sum(k5) / len(k5), min(k5)))

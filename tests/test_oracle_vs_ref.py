@@ -13,7 +13,8 @@ def bits(a):
     return a.view(np.uint32 if a.dtype == np.float32 else np.uint64 if a.dtype == np.float64 else a.dtype)
 
 
-@pytest.mark.parametrize("name", ["desk64", "closed-ped3", "ped5", "linear-regulation", "field-bigger-than-grid", "k16"])
+@pytest.mark.parametrize("name", ["desk64", "closed-ped3", "ped5", "linear-regulation", "field-bigger-than-grid", "k16",
+                                  "sparse-periodic", "sparse-closed", "sparse-field15", "field13-crowd"])
 def test_phase_by_phase(ref_lib, name):
     text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
     ref = shim.Sim.from_scenario(ref_lib, text)
@@ -22,7 +23,7 @@ def test_phase_by_phase(ref_lib, name):
     attrs_ref, attrs_cpu = ref.ped_attrs(), cpu.ped_attrs()
     for key in attrs_ref:
         np.testing.assert_array_equal(attrs_ref[key], attrs_cpu[key], err_msg=key)
-    for tick in range(12):
+    for tick in range(12 if ref.width * ref.height <= 8192 else 4):
         cap = ref.step_capture()
         probe = cpu.clone()
         probe.step(until_phase=4)
