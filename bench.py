@@ -124,7 +124,7 @@ def k5_roofline(workload: str, cells: int, k5_us: float, kernel: str):
 
 
 K5_KERNEL = {"pairs": "k5_pairs_kernel (one launch per tick)", "listwalk": "k5_listwalk_kernel",
-             "window": "k5_window_kernel + dense hand-off", "scatter+gather": "k5_writeback_kernel (scatter / event-walk gather)"}
+             "window": "k5_window_kernel + dense hand-off", "field": "k5_field_kernel (one launch per tick)", "scatter+gather": "k5_writeback_kernel (scatter / event-walk gather)"}
 
 
 class ClockSampler(threading.Thread):

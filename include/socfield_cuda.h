@@ -227,7 +227,7 @@ typedef struct sfc_counters {
     int64_t kernel_launches;
     int64_t graph_launches;
     int64_t h2d_bytes, d2h_bytes;
-    int32_t k5_path;        /* k-5 formulation chosen for the uploaded state: 0 scatter / event-walk gather, 1 window, 2 list walk, 3 pairs */
+    int32_t k5_path;        /* k-5 formulation chosen for the uploaded state: 0 scatter / event-walk gather, 1 window, 2 list walk, 3 pairs, 4 large-field */
     int32_t k5_active_list; /* 1: k-5 visits only the tiles k-4 listed */
 } sfc_counters;
 void sfc_get_counters(const sfc_engine* e, sfc_counters* out);

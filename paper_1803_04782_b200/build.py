@@ -29,7 +29,7 @@ HOST = os.path.join(PKG, "host")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 
-CUDA_SOURCES = ["sfc_api.cu", "sfc_ped_kernels.cu", "sfc_k5_writeback.cu", "sfc_k5_window.cu", "sfc_k5_listwalk.cu", "sfc_k5_pairs.cu", "sfc_rasterize.cu", "sfc_slab.cu", "sfc_digest.cu"]
+CUDA_SOURCES = ["sfc_api.cu", "sfc_ped_kernels.cu", "sfc_k5_writeback.cu", "sfc_k5_window.cu", "sfc_k5_listwalk.cu", "sfc_k5_pairs.cu", "sfc_k5_field.cu", "sfc_rasterize.cu", "sfc_slab.cu", "sfc_digest.cu"]
 HOST_SOURCES = ["model.cpp", "engine.cpp", "raster.cpp", "scenario.cpp"]
 
 NVCC_FLAGS = [

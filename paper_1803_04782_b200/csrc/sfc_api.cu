@@ -92,6 +92,12 @@ struct sfc_engine {
     int pairs_red = 0;        // its RED variant is exact for the uploaded state (sfc_upload)
     int pairs_red_tables = 0; // ... as far as the field magnitudes go (all >= 2^-40: sums are multiples of 2^-115)
     int pairs_red_pref = -1;  // SFC_K5_RED: 0 never, 1 always (tests), -1 when provably exact
+    FieldTables field{};      // tables of the large-field kernel (blob == nullptr: not available for these tables)
+    int k5_field = 0;         // the large-field kernel is the k-5 kernel (chosen in sfc_upload)
+    int field_ctas[2] = {148, 148}; // its persistent grids ([1]: the lazy shape)
+    int field_nk = 0, field_warps = 0; // SFC_K5_FIELD_NK / SFC_K5_FIELD_WARPS: kinds per walk, warps per CTA (0: by shared memory)
+    int field_lazy = 0;       // partials created on first use (chosen in sfc_upload from the crowd density)
+    int field_lazy_pref = -1; // SFC_K5_FIELD_LAZY: 0 never, 1 always, -1 by crowd density
     int sm_count = 148;
     Stager stager;
     bool uploaded = false;
@@ -413,6 +419,13 @@ K5Launch k5_args(sfc_engine* e, int advance) {
     l.pairs_ctas[0] = e->pairs_ctas[0];
     l.pairs_ctas[1] = e->pairs_ctas[1];
     l.pairs_red = e->pairs_red;
+    l.field = e->field;
+    l.field_path = e->k5_field;
+    l.field_ctas[0] = e->field_ctas[0];
+    l.field_ctas[1] = e->field_ctas[1];
+    l.field_nk = e->field_nk;
+    l.field_warps = e->field_warps;
+    l.field_lazy = e->field_lazy;
     l.listwalk_ctas = e->listwalk_ctas;
     l.window_ctas = e->window_ctas;
     return l;
@@ -507,13 +520,16 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
         const std::string path(knob);
-        e->k5_path_pref = path == "window" ? 1 : (path == "listwalk" ? 2 : (path == "pairs" ? 3 : 0));
+        e->k5_path_pref = path == "window" ? 1 : (path == "listwalk" ? 2 : (path == "pairs" ? 3 : (path == "field" ? 4 : 0)));
         e->k5_window_pref = path == "window";
     }
     if (const char* knob = std::getenv("SFC_K5_DENSE")) e->k5_listwalk = std::string(knob) != "gather";
     if (const char* knob = std::getenv("SFC_K5_LIST_CAP")) e->k5_list_cap = std::atoi(knob);
     if (const char* knob = std::getenv("SFC_K5_RED")) e->pairs_red_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
+    if (const char* knob = std::getenv("SFC_K5_FIELD_NK")) e->field_nk = std::atoi(knob) == 3 ? 3 : (std::atoi(knob) == 1 ? 1 : 0);
+    if (const char* knob = std::getenv("SFC_K5_FIELD_WARPS")) e->field_warps = std::atoi(knob) == 8 ? 8 : (std::atoi(knob) == 4 ? 4 : 0);
+    if (const char* knob = std::getenv("SFC_K5_FIELD_LAZY")) e->field_lazy_pref = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;
     e->g.H = cfg->height;
@@ -586,6 +602,19 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
                 if (!ok) return bail(fail(e, SFC_E_CUDA, "cudaMalloc / cudaMemcpy (pair tables)"));
                 pt.blob = dev;
                 e->pairs = pt;
+            }
+            FieldTables ft{};
+            if (cfg->chunk_k >= 2 && cfg->chunk_k <= 16 && build_field_tables(h, cfg->chunk_k, &ft, &blob)) {
+                unsigned char* dev = nullptr;
+                ok = dev_alloc(&dev, (long long)blob.size()) == cudaSuccess;
+                if (ok) e->table_allocs.push_back(dev);
+                ok = ok && cudaMemcpy(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+                if (!ok) return bail(fail(e, SFC_E_CUDA, "cudaMalloc / cudaMemcpy (field tables)"));
+                ft.blob = dev;
+                if (k5_field_supported(ft, cfg->chunk_k, e->field_nk, e->field_warps)) e->field = ft;
+                else if (std::getenv("SFC_K5_STRICT")) std::fprintf(stderr, "sfc: field kernel shape unsupported (k %d nk %d warps %d)\n", cfg->chunk_k, e->field_nk, e->field_warps);
+            } else if (std::getenv("SFC_K5_STRICT")) {
+                std::fprintf(stderr, "sfc: field tables not buildable (n %d hw %d hh %d)\n", h.n, h.hw, h.hh);
             }
         }
     }
@@ -666,6 +695,8 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         cu(prepare_k5_window(cfg->chunk_k, e->tabs, e->k5_window_event_max, e->sm_count, &e->window_ctas), "cudaFuncSetAttribute(k5 window)");
     if (e->k5_tile_rows != kMarkTileH) e->pairs.blob = nullptr;
     if (e->pairs.blob) cu(prepare_k5_pairs(e->pairs, e->sm_count, e->pairs_ctas), "cudaFuncSetAttribute(k5 pairs)");
+    if (e->field.blob)
+        cu(prepare_k5_field(e->field, cfg->chunk_k, e->field_nk, e->field_warps, e->sm_count, e->field_ctas), "cudaFuncSetAttribute(k5 field)");
     cu(prepare_rebuild(e->tabs), "cudaFuncSetAttribute(rebuild)");
     if (rc == SFC_OK) rc = ensure_peds(e, 0);
     if (rc == SFC_OK) rc = ensure_moved(e, 1);
@@ -809,16 +840,28 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         //   else, fields up to 11 x 11   -> the list-walk kernel alone: per-su cost fixed by the field area, at or
         //                                   below the scatter kernel's from corridor densities up, far below for crowds
         //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
+        //   fields beyond 15 x 15        -> the large-field kernel (every tile; sparse crowds: the window kernel)
         const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || e->k5_path_pref < 0);
         const int window = !pairs && e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
-        const int walk_only = !pairs && !window && e->k5_listwalk && (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
-        const bool use = window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse);
-        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs) {
+        const int field = !pairs && !window && e->field.blob != nullptr &&
+                          (e->k5_path_pref == 4 || (e->k5_path_pref < 0 && e->walk.n > 224));
+        const int walk_only = !pairs && !window && !field && e->k5_listwalk &&
+                              (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
+        if (e->k5_path_pref == 4 && !field && std::getenv("SFC_K5_STRICT"))
+            return fail(e, SFC_E_CONFIG, "SFC_K5_PATH=field: the large-field kernel does not support these tables / this shape");
+        const bool use = !field && (window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse));
+        // the field kernel clears its partials per block unless the crowd is thin: expected events per field window
+        const double events_per_window = 2.0 * (double)P * (double)(e->walk.n + 1) / std::max(1.0, (double)e->g.W * (double)e->g.H);
+        const int lazy = field && (e->field_lazy_pref >= 0 ? e->field_lazy_pref : events_per_window < 24.0);
+        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs ||
+            field != e->k5_field || lazy != e->field_lazy) {
             e->marks = use ? m : TileMarks{};
             e->k5_window = window;
             e->k5_listwalk_only = walk_only;
             e->k5_pairs = pairs;
-            e->k5_launches = (walk_only || pairs) ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
+            e->k5_field = field;
+            e->field_lazy = lazy;
+            e->k5_launches = (walk_only || pairs || field) ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
             e->graph_valid = false;
         }
         // the tick counter may restart: forget every epoch stamp
@@ -1395,7 +1438,7 @@ int sfc_compare(sfc_engine* a, sfc_engine* b, sfc_difference* out) {
 
 void sfc_get_counters(const sfc_engine* e, sfc_counters* out) {
     *out = e->counters;
-    out->k5_path = e->k5_pairs ? 3 : (e->k5_listwalk_only ? 2 : (e->k5_window ? 1 : 0));
+    out->k5_path = e->k5_field ? 4 : (e->k5_pairs ? 3 : (e->k5_listwalk_only ? 2 : (e->k5_window ? 1 : 0)));
     out->k5_active_list = e->marks.epoch != nullptr;
 }
 

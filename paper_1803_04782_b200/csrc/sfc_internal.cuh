@@ -224,6 +224,18 @@ struct PairTables {
     uint32_t sect_packed[kKinds]; // sect of kind k fed by sect group g in bits [3g, 3g + 3)
 };
 
+// Tables of the large-field formulation of k-5 (sfc_k5_field.cu), one device blob: one byte
+// (sect group * K + StepCache slot) per support offset, the quadrant-folded magnitude tables (distinct
+// ones only), the orientation-mask word per group.
+struct FieldTables {
+    const unsigned char* blob;
+    int tab_bytes, mag_bytes;
+    int fw, fh, hw, hh;
+    int ms, mag_stride;             // row stride / size of one folded magnitude table, in doubles
+    int mag_of[kKinds];             // magnitude table of kind k
+    uint32_t group_of_sect[kKinds]; // sect group feeding sect s of kind k in bits [3s, 3s + 3)
+};
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize is state of a (function, device) pair shared by every
 // engine of the process: raise it on the CURRENT device when an engine needs more, never lower it.
 struct SmemGrant {
@@ -265,6 +277,11 @@ struct K5Launch {
     int listwalk_ctas;   // k-5: persistent grid of the list-walk kernel for this engine's tables
     int window_ctas;     // k-5: ... of the window kernel
     int pairs_red;       // k-5: image += (float)total as a float reduction at the L2 (no image value can be subnormal)
+    FieldTables field;   // k-5: tables of the large-field kernel (blob == nullptr: not available)
+    int field_path;      // k-5: the large-field kernel is the k-5 kernel
+    int field_ctas[2];   // k-5: its persistent grid ([1]: the lazy shape)
+    int field_nk, field_warps; // k-5: forced kinds per walk / warps per CTA (0: chosen from the shared-memory budget)
+    int field_lazy;      // k-5: partials created on first use (sparse crowds) instead of cleared per block
 };
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab);
@@ -327,6 +344,11 @@ cudaError_t launch_k5_listwalk(cudaStream_t s, const K5Launch& a, bool from_dens
 bool build_pair_tables(const WalkListsHost& w, int chunk_k, PairTables* out, std::vector<unsigned char>* blob);
 cudaError_t prepare_k5_pairs(const PairTables& t, int sm_count, int* ctas);
 cudaError_t launch_k5_pairs(cudaStream_t s, const K5Launch& a);
+// large-field formulation of k-5 (sfc_k5_field.cu)
+bool build_field_tables(const WalkListsHost& w, int chunk_k, FieldTables* out, std::vector<unsigned char>* blob);
+bool k5_field_supported(const FieldTables& t, int chunk_k, int nk_pref, int warps_pref);
+cudaError_t prepare_k5_field(const FieldTables& t, int chunk_k, int nk_pref, int warps_pref, int sm_count, int* ctas);
+cudaError_t launch_k5_field(cudaStream_t s, const K5Launch& a);
 cudaError_t prepare_rebuild(const TablesDev& t);
 // acceptance digest / states_identical on the device (sfc_digest.cu)
 size_t digest_scratch_bytes(long long cells, long long peds);

@@ -748,6 +748,7 @@ cudaError_t prepare_k(const TablesDev& t) {
 template <int K, int SG>
 cudaError_t launch_k(cudaStream_t s, const K5Launch& l) {
     if (l.pairs_path && l.pairs.blob != nullptr) return launch_k5_pairs(s, l);
+    if (l.field_path && l.field.blob != nullptr) return launch_k5_field(s, l);
     const bool walk = l.listwalk && k5_listwalk_supported(l.walk); // dense 32 x 8 tiles: list walk instead of event walk
     if (l.listwalk_only && walk) return launch_k5_listwalk(s, l, false);
     if (l.window_path && k5_window_supported(l.t) && l.dense_list != nullptr) {

@@ -224,6 +224,7 @@ def test_large_field_gather(product_lib, monkeypatch, name, ticks, list_cap):
     gather on 32 x 16 tiles whose field region is staged in column chunks: one sorted event list per
     tile when the events fit, re-staging per walk when they do not (forced with a 16-event list).
     Bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_PATH", "scatter")  # (the default for these fields is the field kernel, below)
     if list_cap:
         monkeypatch.setenv("SFC_K5_LIST_CAP", list_cap)
     text = sc.EXTRA[name]
@@ -232,6 +233,37 @@ def test_large_field_gather(product_lib, monkeypatch, name, ticks, list_cap):
     for step in range(2):
         np.testing.assert_array_equal(gpu.run(ticks // 2), cpu.run(ticks // 2), err_msg=f"{name} moved")
         assert_state_equal(gpu, cpu, f"{name} tick {(step + 1) * (ticks // 2)}")
+
+
+FIELD_VARIANTS = [  # (kinds per walk, warps per CTA, lazy partials, list capacity); None = the engine's choice
+    (None, None, None, None), ("3", "4", "0", None), ("3", "4", "1", None), ("1", "8", "0", None), ("1", "8", "1", None),
+    ("1", "4", "1", "48"), ("3", "4", "0", "48"),
+]
+
+
+@pytest.mark.parametrize("nk,warps,lazy,cap", FIELD_VARIANTS)
+@pytest.mark.parametrize("name", ["desk64", "k2", "k4", "k16", "field-5x9", "field21", "field-bigger-than-grid", "closed-four",
+                                  "closed-ped3", "field35", "field41-crowd", "field13-crowd", "wide-ragged", "sparse-closed",
+                                  "weights", "d0.9-eight-ped1"])
+def test_field_kernel(product_lib, monkeypatch, name, nk, warps, lazy, cap):
+    """The large-field kernel (default beyond 15 x 15: BASELINE configs 3 and 5) forced on fields of
+    every size and crowds of every density, in each of its shapes: three kinds per walk or one, four
+    or eight warps per CTA, partials cleared per block or created lazily, and with a 48-event list
+    so the region streams through many column chunks.  All bit-identical to the oracle."""
+    monkeypatch.setenv("SFC_K5_PATH", "field")
+    for knob, value in (("SFC_K5_FIELD_NK", nk), ("SFC_K5_FIELD_WARPS", warps), ("SFC_K5_FIELD_LAZY", lazy), ("SFC_K5_LIST_CAP", cap)):
+        if value is not None:
+            monkeypatch.setenv(knob, value)
+    monkeypatch.setenv("SFC_K5_STRICT", "1")  # a forced path that cannot be honoured is an error, not a silent fallback
+    if name == "k16" and (nk == "3" or warps == "8"):
+        pytest.skip("sixteen partials per address: one kind per walk only")
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    ticks = 4 if "field4" in name or "field35" in name else 8
+    for step in range(3):
+        np.testing.assert_array_equal(gpu.run(ticks), cpu.run(ticks), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} nk {nk} warps {warps} lazy {lazy} cap {cap} tick {ticks * (step + 1)}")
 
 
 @pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list", "pairs-list"])
