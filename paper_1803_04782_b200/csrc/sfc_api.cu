@@ -528,7 +528,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     if (const char* knob = std::getenv("SFC_K5_RED")) e->pairs_red_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_ACTIVE_LIST")) e->k5_active_list = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_FIELD_NK")) e->field_nk = std::atoi(knob) == 3 ? 3 : (std::atoi(knob) == 1 ? 1 : 0);
-    if (const char* knob = std::getenv("SFC_K5_FIELD_WARPS")) e->field_warps = std::atoi(knob) == 8 ? 8 : (std::atoi(knob) == 4 ? 4 : 0);
+    if (const char* knob = std::getenv("SFC_K5_FIELD_WARPS")) e->field_warps = std::atoi(knob) == 16 ? 16 : (std::atoi(knob) == 8 ? 8 : (std::atoi(knob) == 4 ? 4 : 0));
     if (const char* knob = std::getenv("SFC_K5_FIELD_LAZY")) e->field_lazy_pref = std::atoi(knob) != 0;
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(e, SFC_E_CUDA, "cudaSetDevice failed"));
     e->g.W = cfg->width;

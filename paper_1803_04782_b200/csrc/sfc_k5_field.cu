@@ -4,30 +4,34 @@
 //
 // The reference walks, for every (su, kind, sect) address, that sect's contributor list (F offsets,
 // two mask probes each) and adds the gated terms to K f64 partials: term idx -> partial idx mod K,
-// idx = 2 j (left) / 2 j + 1 (arrived) for list position j; partials folded in slot order, cast to
-// float, added to the image.  Here the non-zero terms are found from the EVENTS instead:
+// idx = 2 j for the "left" term and 2 j + 1 for the "arrived" term of list position j; partials
+// folded in slot order, cast to float, added to the image.  Here the non-zero terms are found from
+// the EVENTS instead:
 //
-//   tile      a CTA of NW warps owns a tile of NW blocks of 8 x 4 su (32 x 4 or 32 x 8 su), one
-//             block per warp, one su per lane, for the whole life of the tile.
+//   tile      a CTA of NW warps owns a tile of NW blocks of 8 x 2 su (32 x 2 / 32 x 4 / 32 x 8 su), one
+//             block per warp for the whole life of the tile.  A su is served by TWO lanes: lane l < 16
+//             adds its "left" terms (even StepCache slots), lane l + 16 its "arrived" terms (odd slots)
+//             — the two never share a partial, so a warp consumes one left event and one arrived event
+//             per step and needs half the partials per lane: twice the warps for the same shared memory.
 //   stage     the tile + field-halo region of the 2-byte event map is read once with 16-byte loads
-//             (eight cells); cells with an event set a bit in a per-column bit map in shared memory.
-//             A popcount scan over the columns gives every event its place in the (x, y)-sorted
-//             event list — the reference's contributor-list order for every su of the tile, because
-//             the lists are sorted lexicographically by centre offset (fields.hpp:55-57).
-//   stream    the list is materialised in column chunks of at most `cap` events (normally one
-//             chunk) and walked by every warp with a WARP-UNIFORM trip count: lanes differ only in
-//             the offset they see.  Per (event, lane): one table byte (sect group * K + StepCache
-//             slot), one orientation-mask word per group, the magnitude from a quadrant-folded f64
-//             table (|dx|, |dy|: the magnitudes are symmetric, checked on the host) — all in shared
-//             memory — then one f64 read-modify-write per gated term on the lane's own partials,
-//             laid out [kind][group][slot][lane] (bank = lane: conflict-free whatever the slot).
-//             The partials persist across chunks, so nothing is ever re-staged; the three kinds
-//             share one walk (NK = 3) when their partials fit, else one walk per kind (NK = 1).
-//   fold      StepCache::total per touched (kind, sect) in slot order, image += (float)total, one
-//             32-byte sector per touched (su, kind).
+//             (eight cells); cells somebody left / arrived at set a bit in per-column bit maps in shared
+//             memory.  A popcount scan over the columns gives every event its place in the (x, y)-sorted
+//             left / arrived event lists — the reference's contributor-list order for every su of the
+//             tile, because the lists are sorted lexicographically by centre offset (fields.hpp:55-57).
+//   stream    the lists are materialised in column chunks of at most `cap` events each (normally one
+//             chunk) and walked by every warp with a WARP-UNIFORM trip count: lanes differ only in the
+//             offset they see.  Per (event, lane): one table byte (sect group * K + StepCache slot), one
+//             orientation-mask word per group, the magnitude from a quadrant-folded f64 table (|dx|,
+//             |dy|: the magnitudes are symmetric, checked on the host) — all in shared memory — then one
+//             f64 read-modify-write per gated term on the lane's own partials, laid out
+//             [kind][group][slot / 2][lane] (bank = lane: conflict-free whatever the slot).  The
+//             partials persist across chunks, so nothing is ever re-staged; the three kinds share one
+//             walk (NK = 3) when their partials fit, else one walk per kind (NK = 1).
+//   fold      StepCache::total per (kind, sect) in slot order — alternating between the su's two lanes'
+//             partials —, image += (float)total; each lane of the pair folds four sects of every kind.
 //
 // Zero terms are never materialised (x + +-0.0 = x), empty partials hold +0.0 (0.0 + p = p, and a
-// partial is never -0.0), so the bits are the reference's.  LAZY variants (sparse crowds) create a
+// partial is never -0.0), so the bits are the reference's.  LAZY variants (thin crowds) create a
 // partial on its first term under a per-lane dirty mask instead of clearing all of them per block.
 // Fields larger than the grid wrap onto themselves: the region is staged in unwrapped coordinates
 // (engine.cpp:450-454).
@@ -42,19 +46,17 @@ namespace sfc {
 
 namespace {
 
-constexpr int kBlockW = 8, kBlockH = 4;
+constexpr int kBlockW = 8, kBlockH = 2;
 constexpr int kTileW = 32;
-constexpr int kMaxThreads = 256;
+constexpr int kMaxThreads = 512;
 constexpr size_t kSmemLimit = 227u << 10;
 constexpr uint32_t kNoEntry = 0xFFu;
 
-// One movement event as the walks see it: a cell somebody LEFT (term -magnitude, StepCache idx 2 j)
-// or ARRIVED at (term +magnitude, idx 2 j + 1).  A cell with both yields two entries.
-struct __align__(16) FieldEvent {
-    uint32_t sel; // one-hot orientation selectors, kind k in byte k (kind 2: bit 16) | arrived << 31
-    int lin;      // ry * fw + rc: the uniform part of the table index
-    int rc, ry;   // region column / row
-};
+// One movement event as the walks see it (8 bytes): a cell somebody LEFT (term -magnitude, StepCache
+// idx 2 j) or ARRIVED at (term +magnitude, idx 2 j + 1) — the two kinds live in separate lists.
+//   x: one-hot orientation selectors, kind k in byte k (kind 2: bit 16) | region row << 17
+//   y: region column
+typedef uint2 FieldEvent;
 
 struct FieldArgs {
     GridDev g;
@@ -69,7 +71,7 @@ struct FieldArgs {
     uint32_t group_of_sect[kKinds]; // sect group feeding sect s of kind k in bits [3s, 3s + 3)
     int tiles_x, n_tiles, tile_h;
     int rw_max, nwords;           // region columns of a full tile; 32-bit words per column bit map
-    int cap;                      // entries per list chunk
+    int cap;                      // entries per list chunk (each of the two lists)
     int advance_tick;
     int vec_ok;                   // 16-byte event-map loads are aligned (W % 8 == 0)
 };
@@ -78,18 +80,13 @@ __device__ __forceinline__ uint32_t selector(uint32_t b) { // one-hot orientatio
     return ((1u << (b & 7u)) | (256u << ((b >> 3) & 7u)) | 0x10000u) * (b >> 7);
 }
 
-template <int K>
-struct Log2K {
-    static constexpr int value = K == 2 ? 1 : (K == 4 ? 2 : (K == 8 ? 3 : 4));
-};
-
-template <int K, int NK, bool LAZY>
+// ONE_MAG: the kinds of a walk share one magnitude table (always true for NK == 1).
+template <int K, int NK, bool LAZY, bool ONE_MAG>
 __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int PW = NK * kSects * K * 32;   // partial doubles per warp
-    constexpr int KO = kSects * K * 32;        // ... per kind
-    constexpr int DW = (kSects * K + 63) / 64; // dirty words per kind
-    constexpr int LOGK = Log2K<K>::value;
+    constexpr int KH = K / 2;                // partials per (kind, group) and lane: the even or the odd slots
+    constexpr int KO = kSects * KH * 32;     // partial doubles per kind and warp
+    constexpr int PW = NK * KO;              // ... per warp
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
     if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
@@ -98,10 +95,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
     // ---- shared memory ------------------------------------------------------------------------
     double* const part_all = reinterpret_cast<double*>(smem_raw);
     double* const smag = part_all + (size_t)NW * PW;
-    FieldEvent* const evl = reinterpret_cast<FieldEvent*>(smag + a.mag_bytes / 8);
-    uint32_t* const colbits = reinterpret_cast<uint32_t*>(evl + a.cap); // [column][left words | arrived words]
-    int* const colstart = reinterpret_cast<int*>(colbits + a.rw_max * 2 * a.nwords);
-    uint32_t* const lut = reinterpret_cast<uint32_t*>(colstart + a.rw_max + 2);
+    FieldEvent* const evl = reinterpret_cast<FieldEvent*>(smag + a.mag_bytes / 8); // [left: cap | arrived: cap]
+    uint32_t* const colbits = reinterpret_cast<uint32_t*>(evl + 2 * a.cap);        // [column][left words | arrived words]
+    int* const colstart = reinterpret_cast<int*>(colbits + a.rw_max * 2 * a.nwords); // [left: rw_max + 2 | arrived: rw_max + 2]
+    uint32_t* const lut = reinterpret_cast<uint32_t*>(colstart + 2 * (a.rw_max + 2));
     uint8_t* const tab8 = reinterpret_cast<uint8_t*>(lut + kSects);
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(a.blob);
@@ -115,10 +112,13 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
 
     const GridDev g = a.g;
     const int HW = a.hw, HH = a.hh, FW = a.fw, MS = a.ms, NWORDS = a.nwords, CW = 2 * a.nwords;
+    const int CS = a.rw_max + 2; // stride between the two column-start arrays
     const uint16_t* const ev16 = reinterpret_cast<const uint16_t*>(a.ev);
     double* const part = part_all + (size_t)warp * PW + lane;
+    const int half = lane >> 4;                        // 0: this lane adds "left" terms, 1: "arrived" terms
     const int bx = (warp & 3) * kBlockW, by = (warp >> 2) * kBlockH;
-    const int sx = lane & 7, sy = lane >> 3;
+    const int sx = lane & 7, sy = (lane >> 3) & 1;
+    const int flip = half ? 0 : (int)0x80000000u;      // left: -magnitude
 
     for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         const int tile_y = tile / a.tiles_x, tile_x = tile - tile_y * a.tiles_x;
@@ -193,26 +193,29 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
             }
         }
         __syncthreads();
-        if (warp == 0) { // exclusive column starts: scan of the per-column entry counts
-            int carry = 0;
-            for (int c0 = 0; c0 < RW; c0 += 32) {
-                const int c = c0 + lane;
-                int v = 0;
-                if (c < RW)
-                    for (int w = 0; w < CW; ++w) v += __popc(colbits[c * CW + w]);
+        if (warp < 2) { // exclusive column starts of the left (warp 0) and arrived (warp 1) lists: popcount scans
+            for (int t = warp; t < 2; t += NW) {
+                int* const cs = colstart + t * CS;
+                int carry = 0;
+                for (int c0 = 0; c0 < RW; c0 += 32) {
+                    const int c = c0 + lane;
+                    int v = 0;
+                    if (c < RW)
+                        for (int w = 0; w < NWORDS; ++w) v += __popc(colbits[c * CW + t * NWORDS + w]);
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                    if (lane >= o) v += u;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                        if (lane >= o) v += u;
+                    }
+                    if (c < RW) cs[c + 1] = v + carry;
+                    carry += __shfl_sync(0xFFFFFFFFu, v, 31);
                 }
-                if (c < RW) colstart[c + 1] = v + carry;
-                carry += __shfl_sync(0xFFFFFFFFu, v, 31);
+                if (lane == 0) cs[0] = 0;
             }
-            if (lane == 0) colstart[0] = 0;
         }
         __syncthreads();
-        const int n_total = colstart[RW];
-        if (n_total == 0) continue; // nobody moved within reach of this tile (uniform; colbits untouched until the next sync)
+        const int n_left = colstart[RW], n_arrived = colstart[CS + RW];
+        if (n_left + n_arrived == 0) continue; // nobody moved within reach of this tile (uniform; colbits untouched until the next sync)
 
         // ---- my block --------------------------------------------------------------------------
         const bool blk_ok = bx < nx && by < ny; // uniform per warp
@@ -220,97 +223,87 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
         const bool in_grid = blk_ok && cx < nx && cy < ny;
         const int tcx = cx + HW, tcy = cy + HH; // my su in region coordinates
         const int col_lo = bx, col_hi = min(bx + kBlockW + 2 * HW, RW); // region columns within the block's reach
-        const bool blk_live = blk_ok && colstart[col_hi] > colstart[col_lo];
-        const bool single = n_total <= a.cap;
-        // table word of the offset (event - my su): tabp[event.lin]; one magnitude row per |dy|
+        const bool blk_live = blk_ok && (colstart[col_hi] > colstart[col_lo] || colstart[CS + col_hi] > colstart[CS + col_lo]);
+        const bool single = n_left <= a.cap && n_arrived <= a.cap;
+        // table byte of the offset (event - my su): tabp[ry * FW + rc]; one magnitude row per |dy|
         const uint8_t* const tabp = tab8 + ((HH - tcy) * FW + (HW - tcx));
         const unsigned span_x = 2u * (unsigned)HW, span_y = 2u * (unsigned)HH;
+        const FieldEvent* const my_list = evl + half * a.cap;
+        const int* const my_cs = colstart + half * CS;
 
 #pragma unroll 1
         for (int kp = 0; kp < kKinds / NK; ++kp) {
-            unsigned long long dirty[NK][DW];
+            unsigned long long dirty[NK]; // LAZY: partials created so far, bit = group * K/2 + slot / 2
             bool any = false;
             const double* mtab[NK]; // kind k's magnitude table
 #pragma unroll
-            for (int k = 0; k < NK; ++k) mtab[k] = smag + a.mag_of[NK == 1 ? kp : k] * a.mag_stride;
-            const bool one_mag = NK == 1 || (mtab[1] == mtab[0] && mtab[2] == mtab[0]); // (uniform)
+            for (int k = 0; k < NK; ++k) {
+                mtab[k] = smag + a.mag_of[NK == 1 ? kp : k] * a.mag_stride;
+                dirty[k] = 0ull;
+            }
             const uint32_t kmask = NK == 3 ? 0x1FFFFu : (kp == 0 ? 0xFFu : (kp == 1 ? 0xFF00u : 0x10000u));
-#pragma unroll
-            for (int k = 0; k < NK; ++k)
-#pragma unroll
-                for (int w = 0; w < DW; ++w) dirty[k][w] = 0ull;
             if (!LAZY && blk_live) {
 #pragma unroll 8
-                for (int i = 0; i < NK * kSects * K; ++i) part[i * 32] = 0.0;
+                for (int i = 0; i < NK * kSects * KH; ++i) part[i * 32] = 0.0;
             }
 
             int c0 = 0;
             while (c0 < RW) {
                 int c1 = RW;
-                const int base = colstart[c0];
-                if (n_total - base > a.cap) {
+                const int base_l = colstart[c0], base_a = colstart[CS + c0];
+                if (n_left - base_l > a.cap || n_arrived - base_a > a.cap) {
                     c1 = c0 + 1;
-                    while (c1 < RW && colstart[c1 + 1] - base <= a.cap) ++c1;
+                    while (c1 < RW && colstart[c1 + 1] - base_l <= a.cap && colstart[CS + c1 + 1] - base_a <= a.cap) ++c1;
                 }
                 if (!(single && kp > 0)) { // (a single chunk is listed once and kept for every kind pass)
-                    if (!single) __syncthreads(); // the previous chunk's walks are done with evl
-                    const int items = (c1 - c0) * NWORDS;
+                    if (!single) __syncthreads(); // the previous chunk's walks are done with the lists
+                    const int items = (c1 - c0) * CW; // (column, left / arrived, word)
                     for (int i = tid; i < items; i += NT) {
-                        const int c = c0 + i / NWORDS, w = i - (c - c0) * NWORDS;
-                        const uint32_t bf = colbits[c * CW + w], bt = colbits[c * CW + NWORDS + w];
-                        uint32_t bits = bf | bt;
+                        const int c = c0 + i / CW, tw = i - (c - c0) * CW, t = tw >= NWORDS ? 1 : 0, w = tw - t * NWORDS;
+                        uint32_t bits = colbits[c * CW + tw];
                         if (bits == 0u) continue;
-                        int pos = colstart[c] - base;
-                        for (int q = 0; q < w; ++q) pos += __popc(colbits[c * CW + q]) + __popc(colbits[c * CW + NWORDS + q]);
+                        int pos = colstart[t * CS + c] - (t ? base_a : base_l);
+                        for (int q = 0; q < w; ++q) pos += __popc(colbits[c * CW + t * NWORDS + q]);
+                        FieldEvent* const out = evl + t * a.cap;
                         while (bits != 0u) {
-                            const int r = __ffs((int)bits) - 1, ry = w * 32 + r;
+                            const int ry = w * 32 + __ffs((int)bits) - 1;
                             bits &= bits - 1u;
                             const long long idx = cell_index(g, xs + c, ys + ry);
                             const uint32_t code = idx >= 0 ? (uint32_t)__ldg(ev16 + idx) : 0u;
-                            FieldEvent fe;
-                            fe.lin = ry * FW + c;
-                            fe.rc = c;
-                            fe.ry = ry;
-                            if ((bf >> r) & 1u) {
-                                fe.sel = selector(code & 0xFFu);
-                                evl[pos++] = fe;
-                            }
-                            if ((bt >> r) & 1u) {
-                                fe.sel = selector(code >> 8) | 0x80000000u;
-                                evl[pos++] = fe;
-                            }
+                            out[pos++] = make_uint2(selector(t ? code >> 8 : code & 0xFFu) | ((uint32_t)ry << 17), (uint32_t)c);
                         }
                     }
                     __syncthreads();
                 }
 
-                // ---- walk the chunk's events within my block's reach ---------------------------
+                // ---- walk the chunk's events within my block's reach: one left and one arrived event per step
                 const int lo = max(c0, col_lo), hi = min(c1, col_hi);
                 if (blk_live && lo < hi) {
-                    const int e0 = colstart[lo] - base, e1 = colstart[hi] - base;
-                    auto lookup = [&](const FieldEvent& fe) -> uint32_t {
-                        const bool ok = in_grid && (unsigned)(fe.rc - tcx + HW) <= span_x && (unsigned)(fe.ry - tcy + HH) <= span_y;
-                        return ok ? (uint32_t)tabp[fe.lin] : kNoEntry;
-                    };
+                    const int my_base = half ? base_a : base_l;
+                    const int e0 = my_cs[lo] - my_base, e1 = my_cs[hi] - my_base;
+                    const int len = e1 - e0;
+                    const int steps = max(__shfl_sync(0xFFFFFFFFu, len, 0), __shfl_sync(0xFFFFFFFFu, len, 16));
 #pragma unroll 1
-                    for (int e = e0; e < e1; e += 2) {
+                    for (int i = 0; i < steps; i += 2) {
                         // two events per trip: both table lookups are in flight before either event's partials are touched
                         FieldEvent fe[2];
                         uint32_t info[2];
-                        fe[0] = evl[e];
-                        fe[1] = evl[min(e + 1, e1 - 1)];
-                        info[0] = lookup(fe[0]);
-                        info[1] = e + 1 < e1 ? lookup(fe[1]) : kNoEntry;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int e = e0 + i + h;
+                            fe[h] = my_list[min(e, a.cap - 1)];
+                            const int u = (int)fe[h].y - tcx, v = (int)(fe[h].x >> 17) - tcy;
+                            const bool ok = e < e1 && in_grid && (unsigned)(u + HW) <= span_x && (unsigned)(v + HH) <= span_y;
+                            info[h] = ok ? (uint32_t)tabp[(int)(fe[h].x >> 17) * FW + (int)fe[h].y] : kNoEntry;
+                        }
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             if (info[h] == kNoEntry) continue;
-                            const FieldEvent cur = fe[h];
-                            const uint32_t gate = lut[info[h] >> LOGK] & cur.sel & kmask; // byte k non-zero: kind k's term is live
+                            const int grp = (int)info[h] / K;
+                            const uint32_t gate = lut[grp] & fe[h].x & kmask; // byte k non-zero: kind k's term is live
                             if (gate == 0u) continue;
-                            const int arrived = (int)(cur.sel >> 31);
-                            const int mi = abs(cur.ry - tcy) * MS + abs(cur.rc - tcx);
-                            const int flip = (int)(~cur.sel & 0x80000000u); // left: -magnitude
-                            const int pidx = (int)info[h] + arrived;        // group * K + slot
+                            const int mi = abs((int)(fe[h].x >> 17) - tcy) * MS + abs((int)fe[h].y - tcx);
+                            const int pidx = (int)(info[h] >> 1); // group * K/2 + slot / 2
                             double* const p = part + pidx * 32;
                             double mk[NK];
                             {
@@ -319,7 +312,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
                             }
 #pragma unroll
                             for (int k = 1; k < NK; ++k) {
-                                if (one_mag) {
+                                if (ONE_MAG) {
                                     mk[k] = mk[0];
                                 } else {
                                     const double m = mtab[k][mi];
@@ -332,16 +325,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
                                 const uint32_t live = NK == 1 ? gate : gate & (k == 0 ? 0xFFu : (k == 1 ? 0xFF00u : 0x10000u));
                                 if (live == 0u) continue;
                                 if (LAZY) {
-                                    const unsigned long long bit = 1ull << (pidx & 63);
-                                    if (DW == 1 || pidx < 64) {
-                                        const double old = (dirty[k][0] & bit) ? p[k * KO] : 0.0;
-                                        p[k * KO] = __dadd_rn(old, mk[k]);
-                                        dirty[k][0] |= bit;
-                                    } else {
-                                        const double old = (dirty[k][DW - 1] & bit) ? p[k * KO] : 0.0;
-                                        p[k * KO] = __dadd_rn(old, mk[k]);
-                                        dirty[k][DW - 1] |= bit;
-                                    }
+                                    const unsigned long long bit = 1ull << pidx;
+                                    const double old = (dirty[k] & bit) ? p[k * KO] : 0.0;
+                                    p[k * KO] = __dadd_rn(old, mk[k]);
+                                    dirty[k] |= bit;
                                 } else {
                                     p[k * KO] = __dadd_rn(p[k * KO], mk[k]);
                                 }
@@ -353,48 +340,56 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
             }
 
             // ---- fold: StepCache::total in slot order, image += (float)total -------------------
-            if (!in_grid || !any) continue;
+            // Slot 2 q lives with the su's "left" lane, slot 2 q + 1 with its "arrived" lane; each lane
+            // of the pair folds four sects of every kind (one 16-byte sector half).
+            const int any_other = __shfl_xor_sync(0xFFFFFFFFu, (int)any, 16);
+            const bool any_su = any || any_other != 0;
+            unsigned long long d_left[NK], d_arrived[NK];
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, dirty[k], 16);
+                d_left[k] = half ? other : dirty[k];
+                d_arrived[k] = half ? dirty[k] : other;
+            }
+            if (!in_grid || !any_su) continue;
             const long long cell = cell_index(g, x0 + cx, y0 + cy);
-            float* const rec = a.dyn + cell * (kKinds * kSects);
+            float* const rec = a.dyn + cell * (kKinds * kSects) + 4 * half;
+            const double* const pl = part - 16 * half; // the pair's "left" lane column (the "arrived" one is 16 further)
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 const int kind = NK == 1 ? kp : k;
-                if (LAZY) {
-                    bool none = true;
-#pragma unroll
-                    for (int w = 0; w < DW; ++w) none = none && dirty[k][w] == 0ull;
-                    if (none) continue;
-                }
+                if (LAZY && (d_left[k] | d_arrived[k]) == 0ull) continue;
                 float4* const r4 = reinterpret_cast<float4*>(rec + kind * kSects);
-                const float4 v0 = r4[0], v1 = r4[1];
-                float r[kSects] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                const uint32_t gos = a.group_of_sect[kind];
+                const float4 v = *r4;
+                float r[4] = {v.x, v.y, v.z, v.w};
+                const uint32_t gos = a.group_of_sect[kind] >> (12 * half);
 #pragma unroll
-                for (int s = 0; s < kSects; ++s) {
-                    const int grp = (int)((gos >> (3 * s)) & 7u);
-                    const double* const p = part + k * KO + grp * (K * 32);
+                for (int j = 0; j < 4; ++j) {
+                    const int grp = (int)((gos >> (3 * j)) & 7u);
+                    const double* const p = pl + k * KO + grp * (KH * 32);
                     double total = 0.0;
                     if (LAZY) {
-                        const int bit0 = grp * K;
-                        const unsigned long long d = (DW == 1 || bit0 < 64) ? dirty[k][0] : dirty[k][DW - 1];
-                        uint32_t gm = (uint32_t)(d >> (bit0 & 63)) & ((1u << K) - 1u);
-                        if (gm == 0u) continue;
-                        while (gm != 0u) { // slot order
-                            const int q = __ffs((int)gm) - 1;
-                            gm &= gm - 1u;
-                            total = __dadd_rn(total, p[q * 32]);
+                        uint32_t ml = (uint32_t)(d_left[k] >> (grp * KH)) & ((1u << KH) - 1u);
+                        uint32_t ma = (uint32_t)(d_arrived[k] >> (grp * KH)) & ((1u << KH) - 1u);
+                        if ((ml | ma) == 0u) continue;
+#pragma unroll
+                        for (int q = 0; q < KH; ++q) { // slot order: 2 q, 2 q + 1
+                            if ((ml >> q) & 1u) total = __dadd_rn(total, p[q * 32]);
+                            if ((ma >> q) & 1u) total = __dadd_rn(total, p[q * 32 + 16]);
                         }
                     } else {
 #pragma unroll
-                        for (int q = 0; q < K; ++q) total = __dadd_rn(total, p[q * 32]);
+                        for (int q = 0; q < KH; ++q) {
+                            total = __dadd_rn(total, p[q * 32]);
+                            total = __dadd_rn(total, p[q * 32 + 16]);
+                        }
                     }
-                    r[s] = __fadd_rn(r[s], __double2float_rn(total)); // engine.cpp:468
+                    r[j] = __fadd_rn(r[j], __double2float_rn(total)); // engine.cpp:468
                 }
-                r4[0] = make_float4(r[0], r[1], r[2], r[3]);
-                r4[1] = make_float4(r[4], r[5], r[6], r[7]);
+                *r4 = make_float4(r[0], r[1], r[2], r[3]);
             }
         }
-        __syncthreads(); // every walk is done before the next tile restages colbits / evl
+        __syncthreads(); // every walk is done before the next tile restages colbits / the lists
     }
 }
 
@@ -408,80 +403,86 @@ struct FieldShape {
 size_t fixed_bytes(const FieldTables& t, int tile_h) {
     const int rw_max = kTileW + 2 * t.hw, rh_max = tile_h + 2 * t.hh;
     const int nwords = (rh_max + 31) / 32;
-    return (size_t)t.mag_bytes + sizeof(uint32_t) * (size_t)rw_max * 2 * nwords + sizeof(int) * (size_t)(rw_max + 2) +
+    return (size_t)t.mag_bytes + sizeof(uint32_t) * (size_t)rw_max * 2 * nwords + sizeof(int) * 2 * (size_t)(rw_max + 2) +
            sizeof(uint32_t) * kSects + (size_t)t.tab_bytes + 16;
 }
 
-// Chooses kinds per walk, warps per CTA and the list capacity for these tables and chunk width:
-// (nk_pref / warps_pref > 0 force a choice; tests and tuning).
+// Chooses kinds per walk, warps per CTA (a warp owns 8 x 2 su: tile height = warps / 2) and the list
+// capacity for these tables and chunk width (nk_pref / warps_pref > 0 force a choice; tests and tuning).
 bool field_shape(const FieldTables& t, int chunk_k, int nk_pref, int warps_pref, bool lazy, FieldShape* out) {
     if (t.blob == nullptr) return false;
     // crowds (partials cleared per block): one walk for the three kinds; thin crowds (lazy partials): the
     // small shape, several CTAs per SM, so one CTA's staging overlaps another's walks
-    static const int eager_order[4][2] = {{3, 4}, {1, 8}, {1, 4}, {3, 8}};
-    static const int lazy_order[4][2] = {{1, 4}, {1, 8}, {3, 4}, {3, 8}};
+    static const int eager_order[6][2] = {{3, 8}, {1, 16}, {1, 8}, {3, 4}, {1, 4}, {3, 16}};
+    static const int lazy_order[6][2] = {{1, 8}, {1, 4}, {1, 16}, {3, 8}, {3, 4}, {3, 16}};
     for (const auto& cand : lazy ? lazy_order : eager_order) {
         const int nk = cand[0], warps = cand[1];
-        if (nk == 3 && chunk_k > 8) continue;
         if (nk_pref > 0 && nk != nk_pref) continue;
         if (warps_pref > 0 && warps != warps_pref) continue;
         const int tile_h = kBlockH * (warps / 4);
-        const size_t part = sizeof(double) * (size_t)warps * nk * kSects * chunk_k * 32;
+        const size_t part = sizeof(double) * (size_t)warps * nk * kSects * (chunk_k / 2) * 32;
         const size_t fixed = fixed_bytes(t, tile_h);
         const int rh_max = tile_h + 2 * t.hh;
-        if (part + fixed + sizeof(FieldEvent) * (size_t)std::max(256, 2 * rh_max) > kSmemLimit) continue;
-        long long cap = (long long)((kSmemLimit - part - fixed) / sizeof(FieldEvent));
+        const size_t per_cap = 2 * sizeof(FieldEvent); // one entry in each of the two lists
+        if (part + fixed + per_cap * (size_t)std::max(128, rh_max) > kSmemLimit) continue;
+        long long cap = (long long)((kSmemLimit - part - fixed) / per_cap);
         const long long region = (long long)(kTileW + 2 * t.hw) * rh_max;
-        // (thin crowds: a short list keeps the CTA small enough for three per SM; longer regions stream in chunks)
-        cap = std::min<long long>(cap, std::min<long long>(2 * region, lazy ? std::max(256, 2 * rh_max) : std::max(1024, 2 * rh_max)));
-        if (cap < 2 * rh_max) continue; // one column must always fit a chunk
+        // (thin crowds: short lists keep the CTA small enough for three per SM; longer regions stream in chunks)
+        cap = std::min<long long>(cap, std::min<long long>(region, lazy ? std::max(256, rh_max) : std::max(1024, rh_max)));
+        if (cap < rh_max) continue; // one column must always fit a chunk
         out->nk = nk;
         out->warps = warps;
         out->tile_h = tile_h;
         out->cap = (int)cap;
         out->rw_max = kTileW + 2 * t.hw;
         out->nwords = (rh_max + 31) / 32;
-        out->smem = (part + fixed + sizeof(FieldEvent) * (size_t)cap + 127) & ~(size_t)127;
+        out->smem = (part + fixed + per_cap * (size_t)cap + 127) & ~(size_t)127;
         return true;
     }
     return false;
 }
 
-template <int K, int NK, bool LAZY>
+template <int K, int NK, bool LAZY, bool ONE_MAG>
 cudaError_t prepare_one(size_t smem, int threads, int sm_count, int* ctas) {
     static SmemGrant grant; // (one per kernel instantiation)
-    cudaError_t e = grant.raise(reinterpret_cast<const void*>(k5_field_kernel<K, NK, LAZY>), smem);
+    cudaError_t e = grant.raise(reinterpret_cast<const void*>(k5_field_kernel<K, NK, LAZY, ONE_MAG>), smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_field_kernel<K, NK, LAZY>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_field_kernel<K, NK, LAZY, ONE_MAG>, threads, smem);
     if (e != cudaSuccess) return e;
     *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
     return cudaSuccess;
 }
 
+bool shares_magnitudes(const FieldTables& t) { return t.mag_of[1] == t.mag_of[0] && t.mag_of[2] == t.mag_of[0]; }
+
 template <int K>
-cudaError_t prepare_k(const FieldShape& sh, bool lazy, int sm_count, int* ctas) {
+cudaError_t prepare_k(const FieldShape& sh, bool lazy, bool one_mag, int sm_count, int* ctas) {
     const int threads = sh.warps * 32;
     if (sh.nk == 3) {
-        if constexpr (K <= 8)
-            return lazy ? prepare_one<K, 3, true>(sh.smem, threads, sm_count, ctas) : prepare_one<K, 3, false>(sh.smem, threads, sm_count, ctas);
-        else
-            return cudaErrorInvalidValue;
+        if (one_mag)
+            return lazy ? prepare_one<K, 3, true, true>(sh.smem, threads, sm_count, ctas)
+                        : prepare_one<K, 3, false, true>(sh.smem, threads, sm_count, ctas);
+        return lazy ? prepare_one<K, 3, true, false>(sh.smem, threads, sm_count, ctas)
+                    : prepare_one<K, 3, false, false>(sh.smem, threads, sm_count, ctas);
     }
-    return lazy ? prepare_one<K, 1, true>(sh.smem, threads, sm_count, ctas) : prepare_one<K, 1, false>(sh.smem, threads, sm_count, ctas);
+    return lazy ? prepare_one<K, 1, true, true>(sh.smem, threads, sm_count, ctas) : prepare_one<K, 1, false, true>(sh.smem, threads, sm_count, ctas);
 }
 
 template <int K>
-void launch_k(cudaStream_t s, const FieldArgs& a, const FieldShape& sh, bool lazy, unsigned blocks) {
+void launch_k(cudaStream_t s, const FieldArgs& a, const FieldShape& sh, bool lazy, bool one_mag, unsigned blocks) {
     const int threads = sh.warps * 32;
     if (sh.nk == 3) {
-        if constexpr (K <= 8) {
-            if (lazy) k5_field_kernel<K, 3, true><<<blocks, threads, sh.smem, s>>>(a);
-            else k5_field_kernel<K, 3, false><<<blocks, threads, sh.smem, s>>>(a);
+        if (one_mag) {
+            if (lazy) k5_field_kernel<K, 3, true, true><<<blocks, threads, sh.smem, s>>>(a);
+            else k5_field_kernel<K, 3, false, true><<<blocks, threads, sh.smem, s>>>(a);
+        } else {
+            if (lazy) k5_field_kernel<K, 3, true, false><<<blocks, threads, sh.smem, s>>>(a);
+            else k5_field_kernel<K, 3, false, false><<<blocks, threads, sh.smem, s>>>(a);
         }
     } else {
-        if (lazy) k5_field_kernel<K, 1, true><<<blocks, threads, sh.smem, s>>>(a);
-        else k5_field_kernel<K, 1, false><<<blocks, threads, sh.smem, s>>>(a);
+        if (lazy) k5_field_kernel<K, 1, true, true><<<blocks, threads, sh.smem, s>>>(a);
+        else k5_field_kernel<K, 1, false, true><<<blocks, threads, sh.smem, s>>>(a);
     }
 }
 
@@ -493,7 +494,7 @@ void launch_k(cudaStream_t s, const FieldArgs& a, const FieldShape& sh, bool laz
 // function of the sect group, a magnitude table is not symmetric, or the field is out of range.
 bool build_field_tables(const WalkListsHost& w, int chunk_k, FieldTables* out, std::vector<unsigned char>* blob) {
     *out = FieldTables{};
-    if (w.n <= 0 || w.hw > 127 || w.hh > 127) return false;
+    if (w.n <= 0 || w.hw > 127 || w.hh > 127) return false; // (list entries: row < 2^15, table index within int)
     const int fw = 2 * w.hw + 1, fh = 2 * w.hh + 1;
     std::vector<uint8_t> tab((size_t)fw * fh, (uint8_t)kNoEntry);
     uint32_t lut[kSects];
@@ -579,10 +580,10 @@ cudaError_t prepare_k5_field(const FieldTables& t, int chunk_k, int nk_pref, int
         if (!field_shape(t, chunk_k, nk_pref, warps_pref, lazy != 0, &sh)) return cudaErrorInvalidValue;
         cudaError_t e = cudaErrorInvalidValue;
         switch (chunk_k) {
-            case 2: e = prepare_k<2>(sh, lazy != 0, sm_count, ctas + lazy); break;
-            case 4: e = prepare_k<4>(sh, lazy != 0, sm_count, ctas + lazy); break;
-            case 8: e = prepare_k<8>(sh, lazy != 0, sm_count, ctas + lazy); break;
-            case 16: e = prepare_k<16>(sh, lazy != 0, sm_count, ctas + lazy); break;
+            case 2: e = prepare_k<2>(sh, lazy != 0, shares_magnitudes(t), sm_count, ctas + lazy); break;
+            case 4: e = prepare_k<4>(sh, lazy != 0, shares_magnitudes(t), sm_count, ctas + lazy); break;
+            case 8: e = prepare_k<8>(sh, lazy != 0, shares_magnitudes(t), sm_count, ctas + lazy); break;
+            case 16: e = prepare_k<16>(sh, lazy != 0, shares_magnitudes(t), sm_count, ctas + lazy); break;
             default: break;
         }
         if (e != cudaSuccess) return e;
@@ -617,17 +618,17 @@ cudaError_t launch_k5_field(cudaStream_t s, const K5Launch& l) {
     a.n_tiles = a.tiles_x * ((l.g.rows + sh.tile_h - 1) / sh.tile_h);
     a.rw_max = sh.rw_max;
     a.nwords = sh.nwords;
-    a.cap = l.list_cap > 0 ? std::clamp(l.list_cap, 2 * (sh.tile_h + 2 * t.hh), sh.cap) : sh.cap;
+    a.cap = l.list_cap > 0 ? std::clamp(l.list_cap, sh.tile_h + 2 * t.hh, sh.cap) : sh.cap;
     a.advance_tick = l.advance_tick;
     a.vec_ok = l.g.W % 8 == 0;
     long long blocks = l.field_ctas[l.field_lazy ? 1 : 0] > 0 ? l.field_ctas[l.field_lazy ? 1 : 0] : 148;
     if (blocks > a.n_tiles) blocks = a.n_tiles;
     if (blocks < 1) blocks = 1;
     switch (l.chunk_k) {
-        case 2: launch_k<2>(s, a, sh, l.field_lazy != 0, (unsigned)blocks); break;
-        case 4: launch_k<4>(s, a, sh, l.field_lazy != 0, (unsigned)blocks); break;
-        case 8: launch_k<8>(s, a, sh, l.field_lazy != 0, (unsigned)blocks); break;
-        case 16: launch_k<16>(s, a, sh, l.field_lazy != 0, (unsigned)blocks); break;
+        case 2: launch_k<2>(s, a, sh, l.field_lazy != 0, shares_magnitudes(t), (unsigned)blocks); break;
+        case 4: launch_k<4>(s, a, sh, l.field_lazy != 0, shares_magnitudes(t), (unsigned)blocks); break;
+        case 8: launch_k<8>(s, a, sh, l.field_lazy != 0, shares_magnitudes(t), (unsigned)blocks); break;
+        case 16: launch_k<16>(s, a, sh, l.field_lazy != 0, shares_magnitudes(t), (unsigned)blocks); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
