@@ -59,6 +59,26 @@ def test_slabs_with_active_tile_list(product_lib, monkeypatch, name, slabs, path
             np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)), err_msg=f"{name} x{slabs} image {k}")
 
 
+@pytest.mark.parametrize("name,slabs", [("desk64", 2), ("field21", 2), ("wide-ragged", 3), ("closed-four", 2), ("field35", 2)])
+@pytest.mark.parametrize("lazy", ["0", "1"])
+def test_slabs_with_field_kernel(product_lib, monkeypatch, name, slabs, lazy):
+    """The large-field kernel on row slabs: its tiles count rows from the slab's first owned row and
+    its regions read the neighbours' events from the halo rows."""
+    monkeypatch.setenv("SFC_SLABS", str(slabs))
+    monkeypatch.setenv("SFC_K5_PATH", "field")
+    monkeypatch.setenv("SFC_K5_STRICT", "1")
+    monkeypatch.setenv("SFC_K5_FIELD_LAZY", lazy)
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for chunk in (1, 5, 9):
+        np.testing.assert_array_equal(gpu.run(chunk), cpu.run(chunk), err_msg=f"{name} x{slabs} moved")
+        np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"{name} x{slabs} tick {gpu.tick} centres")
+        np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"{name} x{slabs} tick {gpu.tick} occupancy")
+        for k in range(3):
+            np.testing.assert_array_equal(bits(gpu.image(k)), bits(cpu.image(k)), err_msg=f"{name} x{slabs} image {k}")
+
+
 def test_slab_halo_too_thin_is_a_config_error(product_lib, monkeypatch):
     monkeypatch.setenv("SFC_SLABS", "8")  # 24 rows / 8 = 3 owned rows < halo 4
     gpu = shim.Sim.from_scenario(product_lib, sc.SEQPAR24)
