@@ -347,10 +347,11 @@ def cpu_reference(w, ticks_per_step: int, steps: int, warmup: int):
 
 
 def bench_slabs(args, w, sf, dist, rank, world, local, warmup):
-    """N > 1: weak scaling over row slabs.  The scenario is the N = 1 workload stacked N times in y
-    (same width, density, fields), so every rank owns the N = 1 amount of su and pedestrians, and
-    the ranks exchange halos with their ring neighbours every tick (paper_1803_04782_b200/slabs.py,
-    NCCL send/recv on the engines' own device buffers)."""
+    """N > 1: the SU grid split into N row slabs, one per GPU, halo exchange with the ring neighbours every
+    tick (paper_1803_04782_b200/slabs.py: NCCL send/recv on the engines' own device buffers, ordered on
+    the engines' streams).  Default: STRONG scaling of BASELINE config 4 (32768^2, 1 M pedestrians) —
+    every rank seeds its own slab on the device, no whole-grid host state exists anywhere.
+    --slab-mode stacked: WEAK scaling, the --workload scenario stacked N times in y."""
     import re
 
     import torch
@@ -358,52 +359,70 @@ def bench_slabs(args, w, sf, dist, rank, world, local, warmup):
     from paper_1803_04782_b200 import slabs
 
     gw, gh = map(int, re.search(r"grid = (\d+)x(\d+)", w["text"]).groups())
-    text = re.sub(r"grid = \d+x\d+", f"grid = {gw}x{gh * world}", w["text"])
+    stacked = args.slab_mode == "stacked"
+    text = re.sub(r"grid = \d+x\d+", f"grid = {gw}x{gh * world}", w["text"]) if stacked else w["text"]
     cfg = sf.parse_scenario(text)
-    state = sf.seed_population(cfg)
-    P, C = state.population, gw * gh * world
-    runner = slabs.SlabRunner(sf, cfg, state, dist, rank, world, local)
+    C = gw * gh * (world if stacked else 1)
+    tps = w.get("ticks_per_step", TICKS_PER_STEP)
+    runner = slabs.SlabRunner(sf, cfg, None, dist, rank, world, local)  # seeds this rank's slab on its GPU
+    P = runner.population
     for _ in range(warmup):
-        runner.run(TICKS_PER_STEP)
+        runner.run(tps)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(dist, local)
     sampler.recording = True
     launches0 = runner.engine.kernel_launches()
-    t0 = time.perf_counter()
+    with torch.cuda.stream(runner.stream):  # CUDA events on the stream the kernels and the NCCL waits are ordered on
+        start.record()
     for _ in range(args.steps):
-        runner.run(TICKS_PER_STEP)  # ends with a stream synchronise
+        runner.run(tps)  # enqueues the whole step; blocks once at its end
+    with torch.cuda.stream(runner.stream):
+        stop.record()
     torch.cuda.synchronize(local)
-    dt = time.perf_counter() - t0
+    dt = start.elapsed_time(stop) * 1e-3
     barrier(dist, local)
     sampler.recording = False
     clocks = sampler.stop()
     dt = reduce_max(dist, local, dt)
+    # end to end: the step plus a device -> host read of the pedestrians' positions (this rank's share)
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier(dist, local)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        runner.run(tps)
+        runner.engine.download_centers(P)
+    barrier(dist, local)
+    e2e_s = reduce_max(dist, local, time.perf_counter() - t0)
     if rank != 0:
         return 0
-    ticks = TICKS_PER_STEP * args.steps
+    ticks = tps * args.steps
     value = P * ticks / dt
     peak, peak_src = measured_peaks()
     tick_gbs = (BYTES_PER_SU_TICK * C + BYTES_PER_PED_TICK * P) / (dt / ticks) / 1e9
     line = {
         "metric": "pedestrian-steps/s", "value": value, "unit": "pedestrian-steps/s", "su_updates_per_s": value * C / P,
         "n_gpus": world, "steps": args.steps, "warmup": warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if stacked else "strong", "vs_baseline": None,
         "dtype": "f64 scores and field sums, f32 field images, i32 occupancy",
         "data": "synthetic (seeded scenario, seed 42)",
-        "config": {"workload": w["label"] + f" — stacked {world}x in y ({gw}x{gh * world} su, {P} pedestrians)",
-                   "ticks_per_step": TICKS_PER_STEP, "cells": C, "pedestrians": P,
-                   "parallelism": f"{world} row slabs, one per GPU, halo exchange per tick ({dist.get_backend()} send/recv)",
-                   "timing": "host-driven tick loop: wall clock between barriers with device synchronisation, max over ranks",
-                   "l2": "per-GPU working set as at N = 1 (134 MB vs 126 MB L2)"},
+        "config": {"workload": w["label"] + (f" — stacked {world}x in y ({gw}x{gh * world} su, {P} pedestrians)" if stacked else ""),
+                   "ticks_per_step": tps, "cells": C, "pedestrians": P,
+                   "parallelism": f"{world} row slabs, one per GPU, halo exchange per tick ({dist.get_backend()} send/recv, "
+                                  "stream-ordered: one host synchronisation per step)",
+                   "timing": "CUDA events on the engine stream around the timed steps, max over ranks",
+                   "l2": "per-GPU working set far above the 126 MB L2; k-5 touches only su within reach of a mover"},
         "clocks": clocks,
-        "e2e": {"value": None, "unit": "pedestrian-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                "note": "measured at N = 1 only: the host-facing call scatters one whole-grid SimState"},
+        "e2e": {"value": P * tps * e2e_steps / e2e_s, "unit": "pedestrian-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 8 * P * world,
+                "call": f"SlabRunner.run({tps}) + SlabEngine.download_centers() on every rank (the 141 GB SimState is never on a host)"},
         "gpu_launches": runner.engine.kernel_launches() - launches0,  # rank 0's kernels in the timed region
         "tick_us": 1e6 * dt / ticks,
         "roofline": {"bound": "hbm", "kernel": "whole tick, all ranks", "achieved": tick_gbs, "peak": peak * world,
-                     "unit": "GB/s", "frac": tick_gbs / (peak * world), "traffic": None, "peak_source": peak_src},
+                     "unit": "GB/s", "frac": tick_gbs / (peak * world), "traffic": None, "peak_source": peak_src,
+                     "note": "algorithmic bytes 200 B per su and per pedestrian (SURVEY 8d); a sparse crowd moves far fewer"},
         "cpu_baseline": None,
     }
     print(json.dumps(line))
@@ -419,9 +438,14 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the `configs` block (the other BASELINE configs) and the parity report")
+    ap.add_argument("--slab-mode", default="c4", choices=["c4", "stacked"],
+                    help="N > 1: 'c4' = strong scaling of BASELINE config 4 over N row slabs (default), "
+                         "'stacked' = weak scaling, the --workload scenario stacked N times in y")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: run the N > 1 slab path with every rank on GPU 0 (single-GPU smoke test of that path)")
     args = ap.parse_args()
+    if args.gpus > 1 and args.impl == "ours" and args.slab_mode == "c4":
+        args.workload = "c4"  # BASELINE config 4 is the multi-GPU configuration (spatial slabs at 2 / 4 / 8 GPUs)
     w = WORKLOADS[args.workload]
     global TICKS_PER_STEP, REF_TICKS_PER_STEP
     TICKS_PER_STEP = w.get("ticks_per_step", TICKS_PER_STEP)

@@ -200,6 +200,10 @@ int sfc_slab_halo_rows(int field_half_h, int ped_half_h, int density_radius_if_r
 int sfc_slab_begin(sfc_engine* e, int64_t ticks);
 int sfc_slab_step(sfc_engine* e, int step);
 int sfc_slab_buffer(sfc_engine* e, int kind, int edge, int recv, void** ptr, size_t* bytes);
+/* The CUDA stream (cudaStream_t) every kernel of this engine is enqueued on: a transport that orders its
+ * sends / receives on it (NCCL under a torch ExternalStream, peer copies with events) keeps the tick loop
+ * free of host synchronisation — the reference's phase barrier (thread_pool.hpp:13-16) becomes stream order. */
+void* sfc_stream(sfc_engine* e);
 /* Synchronises, reports a device-side error, returns TickMetrics::moved of ticks [first, first+ticks)
  * counted since sfc_slab_begin (this slab's movers only). */
 int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* moved);

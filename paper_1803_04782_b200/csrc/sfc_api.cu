@@ -43,6 +43,7 @@ struct sfc_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    cudaEvent_t ev_step = nullptr, ev_copy = nullptr; // slab groups: "my step is enqueued-complete" / "the halo copies into me are"
 
     long long cells = 0; // resident su (slab rows + halos)
     int* occ = nullptr;
@@ -736,6 +737,8 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->dbg.moved_to);
     cudaFree(e->dbg.from_mask);
     cudaFree(e->dbg.to_mask);
+    if (e->ev_step) cudaEventDestroy(e->ev_step);
+    if (e->ev_copy) cudaEventDestroy(e->ev_copy);
     if (e->ev_start) cudaEventDestroy(e->ev_start);
     if (e->ev_stop) cudaEventDestroy(e->ev_stop);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -1258,6 +1261,8 @@ int sfc_slab_buffer(sfc_engine* e, int kind, int edge, int recv, void** ptr, siz
     return SFC_OK;
 }
 
+void* sfc_stream(sfc_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
 int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* moved) {
     SFC_CUDA(cudaSetDevice(e->device));
     std::vector<unsigned long long> m((size_t)std::max<int64_t>(ticks, 0));
@@ -1295,26 +1300,32 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
         const int rc = sfc_slab_begin(engines[i], ticks);
         if (rc != SFC_OK) return rc;
     }
-    auto sync_all = [&]() -> cudaError_t {
-        for (int i = 0; i < n; ++i) {
-            cudaSetDevice(engines[i]->device);
-            const cudaError_t c = cudaStreamSynchronize(engines[i]->stream);
-            if (c != cudaSuccess) return c;
-        }
-        return cudaSuccess;
-    };
-    auto exchange = [&](int kind) -> int { // my edge -> the facing edge of the ring neighbour
+    // Stream-ordered: the host only enqueues.  A copy into slab j waits (event) for the sending slab's
+    // step; a slab's next step waits for the copies into it (same stream) and for the copies its
+    // neighbours took FROM it (their "copies enqueued" events) — nothing blocks the host until finish.
+    for (int i = 0; i < n; ++i) {
+        sfc_engine* e = engines[i];
+        cudaSetDevice(e->device);
+        if (!e->ev_step && cudaEventCreateWithFlags(&e->ev_step, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(e0, cudaGetLastError(), "cudaEventCreate(slab step)");
+        if (!e->ev_copy && cudaEventCreateWithFlags(&e->ev_copy, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(e0, cudaGetLastError(), "cudaEventCreate(slab copy)");
+    }
+    auto neighbour_of = [&](int i, int edge) { return engines[(i + (edge == 0 ? n - 1 : 1)) % n]; };
+    auto exchange = [&](int kind) -> int { // my edge -> the facing edge of the ring neighbour, on the neighbour's stream
         for (int i = 0; i < n; ++i) {
             sfc_engine* e = engines[i];
             for (int edge = 0; edge < 2; ++edge) {
                 if (!slab_has_neighbour(e, edge)) continue;
-                sfc_engine* nb = engines[(i + (edge == 0 ? n - 1 : 1)) % n];
+                sfc_engine* nb = neighbour_of(i, edge);
                 void *src = nullptr, *dst = nullptr;
                 size_t sb = 0, db = 0;
                 int rc = sfc_slab_buffer(e, kind, edge, 0, &src, &sb);
                 if (rc == SFC_OK) rc = sfc_slab_buffer(nb, kind, 1 - edge, 1, &dst, &db);
                 if (rc != SFC_OK || sb != db) return fail(e, SFC_E_STATE, "halo buffers of neighbouring slabs do not match");
-                const cudaError_t c = cudaMemcpyPeerAsync(dst, nb->device, src, e->device, sb, nb->stream);
+                cudaSetDevice(nb->device);
+                cudaError_t c = cudaStreamWaitEvent(nb->stream, e->ev_step, 0);
+                if (c == cudaSuccess) c = cudaMemcpyPeerAsync(dst, nb->device, src, e->device, sb, nb->stream);
                 if (c != cudaSuccess) return cuda_fail(e, c, "cudaMemcpyPeerAsync(halo)");
             }
         }
@@ -1325,20 +1336,26 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
             for (int i = 0; i < n; ++i) {
                 const int rc = sfc_slab_step(engines[i], step);
                 if (rc != SFC_OK) return rc;
+                const cudaError_t c = cudaEventRecord(engines[i]->ev_step, engines[i]->stream);
+                if (c != cudaSuccess) return cuda_fail(e0, c, "cudaEventRecord(slab step)");
             }
-            cudaError_t c = sync_all();
-            if (c != cudaSuccess) return cuda_fail(e0, c, "slab step");
-            if (step == 0) {
-                const int rc = exchange(0);
+            if (step == 2) continue;
+            for (int kind = (step == 0 ? 0 : 1); kind <= (step == 0 ? 0 : 3); ++kind) {
+                const int rc = exchange(kind);
                 if (rc != SFC_OK) return rc;
-            } else if (step == 1) {
-                for (int kind = 1; kind <= 3; ++kind) {
-                    const int rc = exchange(kind);
-                    if (rc != SFC_OK) return rc;
-                }
             }
-            c = sync_all();
-            if (c != cudaSuccess) return cuda_fail(e0, c, "halo exchange");
+            for (int i = 0; i < n; ++i) {
+                cudaSetDevice(engines[i]->device);
+                const cudaError_t c = cudaEventRecord(engines[i]->ev_copy, engines[i]->stream);
+                if (c != cudaSuccess) return cuda_fail(e0, c, "cudaEventRecord(halo copies)");
+            }
+            for (int i = 0; i < n; ++i) // my next step may overwrite what the neighbours are still reading
+                for (int edge = 0; edge < 2; ++edge) {
+                    if (!slab_has_neighbour(engines[i], edge)) continue;
+                    cudaSetDevice(engines[i]->device);
+                    const cudaError_t c = cudaStreamWaitEvent(engines[i]->stream, neighbour_of(i, edge)->ev_copy, 0);
+                    if (c != cudaSuccess) return cuda_fail(e0, c, "cudaStreamWaitEvent(halo copies)");
+                }
         }
     }
     int status = SFC_OK;

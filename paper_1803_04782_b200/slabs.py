@@ -104,6 +104,7 @@ class SlabRunner:
                     ptr, nbytes = self.engine.buffer(kind, edge, recv)
                     self.bufs[kind, edge, recv] = device_tensor(ptr, nbytes, self.device)
         self.torch = torch
+        self.stream = torch.cuda.ExternalStream(self.engine.stream(), device=self.device)
         self.host = {key: torch.empty(t.shape, dtype=t.dtype).pin_memory() for key, t in self.bufs.items()} if self.stage else {}
 
     def _exchange(self, kinds) -> None:
@@ -125,19 +126,34 @@ class SlabRunner:
         exchange(self.dist, self.rank, self.world, self.closed, send, recv)
 
     def run(self, ticks: int):
-        """Advance `ticks` ticks; returns this slab's movers per tick."""
+        """Advance `ticks` ticks; returns this slab's movers per tick.
+
+        NCCL transport: the sends / receives are issued with the engine's own CUDA stream current
+        (torch.cuda.ExternalStream), so NCCL orders them after the step that filled the buffers and
+        `work.wait()` makes the next step wait on that stream — the host only enqueues and blocks once,
+        in `finish`.  Host-staged transport (gloo; tests): the buffers bounce through pinned memory,
+        which needs the stream drained around every exchange."""
         eng, torch = self.engine, self.torch
         eng.begin(ticks)
-        for _ in range(ticks):
-            eng.step(0)
-            eng.finish(0, 0)          # engine stream -> host: the send buffers are complete
-            self._exchange((0,))
-            torch.cuda.synchronize(self.device)
-            eng.step(1)
-            eng.finish(0, 0)
-            self._exchange((1, 2, 3))
-            torch.cuda.synchronize(self.device)
-            eng.step(2)
+        if self.stage:
+            for _ in range(ticks):
+                eng.step(0)
+                eng.finish(0, 0)          # engine stream -> host: the send buffers are complete
+                self._exchange((0,))
+                torch.cuda.synchronize(self.device)
+                eng.step(1)
+                eng.finish(0, 0)
+                self._exchange((1, 2, 3))
+                torch.cuda.synchronize(self.device)
+                eng.step(2)
+            return eng.finish(0, ticks)
+        with torch.cuda.stream(self.stream):
+            for _ in range(ticks):
+                eng.step(0)
+                self._exchange((0,))
+                eng.step(1)
+                self._exchange((1, 2, 3))
+                eng.step(2)
         return eng.finish(0, ticks)
 
     def download(self, state) -> None:
