@@ -59,7 +59,9 @@ struct sfc_engine {
     float* stage = nullptr; // staging for layout conversion
     long long stage_cells = 0;
 
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph = nullptr;       // one tick: k-2, k-3, k-4, k-5
+    cudaGraphExec_t graph_multi = nullptr; // graph_ticks ticks back to back (launch-bound configs: one launch, not graph_ticks)
+    int graph_ticks = 10;                  // SFC_GRAPH_TICKS (1: single-tick graphs only)
     bool graph_valid = false;
 
     // row-slab mode (multi-GPU): halo exchange buffers, [edge 0 = low-y, 1 = high-y][kind 0 = decisions, 1 = positions]
@@ -458,24 +460,35 @@ int enqueue_rebuild(sfc_engine* e) { // maybe_rebuild body, engine.cpp:540-549
     return SFC_OK;
 }
 
-int build_graph(sfc_engine* e) {
-    if (e->graph_valid) return SFC_OK;
-    if (e->graph) {
-        cudaGraphExecDestroy(e->graph);
-        e->graph = nullptr;
-    }
+int capture_ticks(sfc_engine* e, int ticks, cudaGraphExec_t* out) {
     cudaGraph_t graph = nullptr;
     SFC_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-    const int rc = enqueue_tick_kernels(e);
+    int rc = SFC_OK;
+    for (int t = 0; t < ticks && rc == SFC_OK; ++t) rc = enqueue_tick_kernels(e);
     cudaError_t c = cudaStreamEndCapture(e->stream, &graph);
     if (rc != SFC_OK) {
         if (graph) cudaGraphDestroy(graph);
         return rc;
     }
     if (c != cudaSuccess) return cuda_fail(e, c, "cudaStreamEndCapture");
-    c = cudaGraphInstantiate(&e->graph, graph, 0);
+    c = cudaGraphInstantiate(out, graph, 0);
     cudaGraphDestroy(graph);
     if (c != cudaSuccess) return cuda_fail(e, c, "cudaGraphInstantiate");
+    return SFC_OK;
+}
+
+// The tick as CUDA graphs: every kernel reads the tick from the device-resident Ctl, so a captured
+// graph replays tick after tick — and graph_ticks ticks captured back to back replay as one launch.
+int build_graph(sfc_engine* e) {
+    if (e->graph_valid) return SFC_OK;
+    for (cudaGraphExec_t* g : {&e->graph, &e->graph_multi})
+        if (*g) {
+            cudaGraphExecDestroy(*g);
+            *g = nullptr;
+        }
+    int rc = capture_ticks(e, 1, &e->graph);
+    if (rc == SFC_OK && e->graph_ticks > 1) rc = capture_ticks(e, e->graph_ticks, &e->graph_multi);
+    if (rc != SFC_OK) return rc;
     e->graph_valid = true;
     return SFC_OK;
 }
@@ -518,6 +531,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     };
     e->cfg = *cfg;
     e->device = cfg->device;
+    if (const char* knob = std::getenv("SFC_GRAPH_TICKS")) e->graph_ticks = std::clamp(std::atoi(knob), 1, 64);
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
         const std::string path(knob);
@@ -711,6 +725,7 @@ void sfc_destroy(sfc_engine* e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->graph) cudaGraphExecDestroy(e->graph);
+    if (e->graph_multi) cudaGraphExecDestroy(e->graph_multi);
     for (void* p : e->table_allocs) cudaFree(p);
     free_peds(e);
     cudaFree(e->occ);
@@ -965,9 +980,10 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
         if (rc != SFC_OK) return rc;
     }
     SFC_CUDA(cudaEventRecord(e->ev_start, e->stream));
-    for (long long t = 0; t < ticks; ++t) {
+    for (long long t = 0; t < ticks;) {
         rc = erase_marks_if_due(e, base + t);
         if (rc != SFC_OK) return rc;
+        long long done = 1;
         if (with_phase_times) {
             const DebugArrays none{};
             cudaEvent_t* ev = &evs[(size_t)t * 5];
@@ -983,11 +999,18 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 1)));
             if (t == ticks - 1) SFC_CUDA(cudaEventRecord(evs[(size_t)ticks * 5], e->stream));
         } else {
-            SFC_CUDA(cudaGraphLaunch(e->graph, e->stream));
+            // graph_ticks ticks in one launch when no rebuild and no stamp erasure falls strictly inside them
+            const long long n = e->graph_ticks;
+            bool multi = e->graph_multi != nullptr && t + n <= ticks;
+            if (multi && interval > 0 && (base + t) % interval + n > interval) multi = false;
+            if (multi && e->marks_alloc.epoch && (base + t) / (long long)kEpochPeriod != (base + t + n - 1) / (long long)kEpochPeriod) multi = false;
+            if (multi) done = n;
+            SFC_CUDA(cudaGraphLaunch(multi ? e->graph_multi : e->graph, e->stream));
             e->counters.graph_launches += 1;
         }
-        e->counters.kernel_launches += 3 + e->k5_launches;
-        if (interval > 0 && (base + t + 1) % interval == 0) {
+        e->counters.kernel_launches += done * (3 + e->k5_launches);
+        t += done;
+        if (interval > 0 && (base + t) % interval == 0) {
             rc = enqueue_rebuild(e);
             if (rc != SFC_OK) return rc;
         }
