@@ -59,6 +59,8 @@ typedef struct sfc_config {
      * slab_rows = 0 means the whole grid. */
     int32_t slab_row0, slab_rows;
     int32_t slab_halo;             /* resident rows beyond each slab edge (see sfc_slab_halo_rows) */
+    /* > 1: band-swapped engine (sfc_band_run): slab_rows is the band height, the window moves over the grid */
+    int32_t bands;
 } sfc_config;
 
 /* Merged contributor table of one dynamic kind, replacing Engine::build_gather_tables
@@ -210,6 +212,26 @@ int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* m
 /* Single-process driver: runs `ticks` ticks over n slab engines (ordered by slab_row0), exchanging
  * halos with peer copies.  metrics: NULL or [ticks] (moved summed over slabs). */
 int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* metrics);
+
+/* ---- Band-swapped pass: a state LARGER than device memory (the paper's divide-and-conquer against
+ * global-memory depletion; reference accumulator.hpp:68-83 multi_step_sum,
+ * bench.cpp:14-24 memory_plan).  The reference holds one SimState in host memory; here that host
+ * state is the backing store and the SU grid streams through the device in `bands` row bands of
+ * slab_rows rows (+ slab_halo rows each side), one phase at a time:
+ *   pass A  k-2   per band: occupancy (with halo), static + dynamic images in -> decisions
+ *   pass B  k-3   per band: occupancy in -> vote results
+ *   pass C  k-4   per band: occupancy, event map in -> moved, both out (halo rows included: a mover
+ *                 that crosses a band edge writes into the neighbour's rows; bands run in order, so
+ *                 the neighbour loads those rows after the store)
+ *   pass D  k-5   per band: event map (with field halo), dynamic images in -> images out
+ *   rebuild       check pass over every band, verdict, commit pass over every band
+ * Pedestrians (31 B each) stay resident for the whole run, so no pedestrian halo exchange exists.
+ * The engine must have been created with sfc_config.bands > 1; `host` holds every dense array
+ * (occupancy, static_image, dyn_images) and is updated in place; results are bit-identical to sfc_run
+ * on the undivided grid.  sfc_band_plan returns the smallest band count whose window (134 B per
+ * resident su) plus the population fits `device_bytes` (0: what cudaMemGetInfo reports free). */
+int sfc_band_run(sfc_engine* e, sfc_state_view* host, int64_t ticks, sfc_tick_metrics* metrics);
+int sfc_band_plan(int32_t width, int32_t height, int32_t halo, int64_t n_peds, int64_t device_bytes, int device);
 
 /* ---- Validation without host copies.
  * sfc_digest: the acceptance digest of the resident state — FNV-1a over occupancy, the three dynamic

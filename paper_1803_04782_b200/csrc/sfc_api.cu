@@ -70,6 +70,9 @@ struct sfc_engine {
     HaloRecord* halo_recv[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     int halo_capacity = 0; // records per buffer, header included
     int ped_half_h = 0;    // largest pedestrian half-height of the uploaded population
+    int band_count = 0;    // > 1: band-swapped engine (sfc_band_run): g.row0 / g.rows move over the grid
+    int band_rows = 0;     // rows of a full band (the last band may be shorter)
+    std::vector<uint8_t> band_ev; // host backing of the event map (2 B per su of the whole grid)
     int* dense_list = nullptr; // k-5 tile ids handed from the scatter to the gather kernel
     int persistent_ctas = 148 * 3;
     int k5_launches = 1;       // kernels per k-5 phase
@@ -493,6 +496,80 @@ int build_graph(sfc_engine* e) {
     return SFC_OK;
 }
 
+// Packs the pedestrian attributes on the host (cheap, one pass) and enqueues the copies of the per-pedestrian
+// arrays; the staging vectors must outlive the next synchronisation of the engine's stream.
+int upload_peds(sfc_engine* e, const sfc_state_view* v, std::vector<int2>* gate, std::vector<uint32_t>* attr, int* max_hh_out) {
+    const long long P = v->n_peds;
+    gate->resize((size_t)P);
+    attr->resize((size_t)P);
+    int max_hh = 0;
+    for (long long i = 0; i < P; ++i) {
+        const int hw = (v->foot_w[i] - 1) / 2, hh = (v->foot_h[i] - 1) / 2;
+        if (hw > kMaxHalfExtent || hh > kMaxHalfExtent || hw < 0 || hh < 0)
+            return fail(e, SFC_E_CONFIG, "footprint: pedestrian footprint exceeds the device limit (4095)");
+        max_hh = std::max(max_hh, hh);
+        (*gate)[(size_t)i] = make_int2(v->walk_period[i], v->walk_phase[i]);
+        (*attr)[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
+    }
+    *max_hh_out = max_hh;
+    if (P > 0) {
+        SFC_CUDA(cudaMemcpyAsync(e->peds.center, v->center_xy, sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemcpyAsync(e->peds.gate, gate->data(), sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemcpyAsync(e->peds.attr, attr->data(), sizeof(uint32_t) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.dir, 0xFF, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.moved_dir, 0xFF, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.won, 0, (size_t)P, e->stream));
+        SFC_CUDA(cudaMemsetAsync(e->peds.score, 0, sizeof(double) * (size_t)P, e->stream));
+        e->counters.h2d_bytes += (int64_t)((sizeof(int2) * 2 + sizeof(uint32_t)) * P);
+    }
+    return SFC_OK;
+}
+
+// Chooses the k-5 formulation for a population of P pedestrians (all bit-identical; measured in
+// profiles/README.md).  allow_list: the active-tile list (and the window kernel that needs it) may be used.
+int select_k5_path(sfc_engine* e, long long P, bool allow_list) {
+    if (e->marks_alloc.epoch) {
+        // The list pays when most tiles see no mover in a tick: a mover's field box overlaps about
+        // (w/32 + 1) x (h/8 + 1) tiles, every pedestrian may move.  Dense crowds skip the bookkeeping.
+        const TileMarks& m = e->marks_alloc;
+        const long long per_mover = (long long)((2 * m.hw + 1) / kMarkTileW + 2) * ((2 * m.hh + 1) / kMarkTileH + 2);
+        const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
+        const bool sparse = allow_list && P * per_mover < 2 * n_tiles; // (expected share of active tiles below ~85 %)
+        // Which k-5 formulation (all bit-identical; measured in profiles/README.md):
+        //   sparse crowd                 -> window kernel over the active-tile list (dense tiles: list walk / gather)
+        //   else, fields up to 11 x 11   -> the list-walk kernel alone: per-su cost fixed by the field area, at or
+        //                                   below the scatter kernel's from corridor densities up, far below for crowds
+        //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
+        //   fields beyond 15 x 15        -> the large-field kernel (every tile; sparse crowds: the window kernel)
+        const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || e->k5_path_pref < 0);
+        const int window = allow_list && !pairs && e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
+        const int field = !pairs && !window && e->field.blob != nullptr &&
+                          (e->k5_path_pref == 4 || (e->k5_path_pref < 0 && e->walk.n > 224));
+        const int walk_only = !pairs && !window && !field && e->k5_listwalk &&
+                              (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
+        if (e->k5_path_pref == 4 && !field && std::getenv("SFC_K5_STRICT"))
+            return fail(e, SFC_E_CONFIG, "SFC_K5_PATH=field: the large-field kernel does not support these tables / this shape");
+        const bool use = allow_list && !field && (window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse));
+        // the field kernel clears its partials per block unless the crowd is thin: expected events per field window
+        const double events_per_window = 2.0 * (double)P * (double)(e->walk.n + 1) / std::max(1.0, (double)e->g.W * (double)e->g.H);
+        const int lazy = field && (e->field_lazy_pref >= 0 ? e->field_lazy_pref : events_per_window < 24.0);
+        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs ||
+            field != e->k5_field || lazy != e->field_lazy) {
+            e->marks = use ? m : TileMarks{};
+            e->k5_window = window;
+            e->k5_listwalk_only = walk_only;
+            e->k5_pairs = pairs;
+            e->k5_field = field;
+            e->field_lazy = lazy;
+            e->k5_launches = (walk_only || pairs || field) ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
+            e->graph_valid = false;
+        }
+        // the tick counter may restart: forget every epoch stamp
+        SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(unsigned) * (size_t)n_tiles, e->stream));
+    }
+    return SFC_OK;
+}
+
 } // namespace
 
 extern "C" {
@@ -552,6 +629,13 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->g.row0 = cfg->slab_rows > 0 ? cfg->slab_row0 : 0;
     e->g.rows = cfg->slab_rows > 0 ? cfg->slab_rows : cfg->height;
     e->g.halo = 0;
+    if (cfg->bands > 1) { // band-swapped engine: the slab window moves over the grid (sfc_band_run)
+        if (cfg->slab_rows < 1 || cfg->slab_rows >= cfg->height || cfg->slab_row0 != 0)
+            return bail(fail(e, SFC_E_CONFIG, "bands: need 1 <= slab_rows < height and slab_row0 = 0"));
+        e->band_count = cfg->bands;
+        e->band_rows = cfg->slab_rows;
+        e->slab.band = 1;
+    }
     if (e->g.rows != cfg->height) { // a proper row slab: resident rows = owned + halo on both sides
         e->slab.active = 1;
         e->g.halo = cfg->slab_halo;
@@ -672,7 +756,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
         e->k5_window_event_max = (int)std::clamp<long long>(9 * region / (2 * window), 8, 1 << 20);
     }
     if (const char* knob = std::getenv("SFC_K5_EVENT_MAX")) e->k5_event_max = e->k5_window_event_max = std::atoi(knob);
-    if (e->slab.active) {
+    if (e->slab.active && !e->slab.band) {
         const long long band = (long long)e->g.W * (2 * e->g.halo) + 1;
         e->halo_capacity = (int)std::min<long long>(band, 1 << 18);
         for (int edge = 0; edge < 2; ++edge)
@@ -778,18 +862,9 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
     if (rc != SFC_OK) return rc;
     rc = ensure_stage(e);
     if (rc != SFC_OK) return rc;
-    // pedestrian attributes: pack on the host (cheap, one pass), copy once
-    std::vector<int2> gate((size_t)P);
-    std::vector<uint32_t> attr((size_t)P);
+    std::vector<int2> gate;
+    std::vector<uint32_t> attr;
     int max_hh = 0;
-    for (long long i = 0; i < P; ++i) {
-        const int hw = (v->foot_w[i] - 1) / 2, hh = (v->foot_h[i] - 1) / 2;
-        if (hw > kMaxHalfExtent || hh > kMaxHalfExtent || hw < 0 || hh < 0)
-            return fail(e, SFC_E_CONFIG, "footprint: pedestrian footprint exceeds the device limit (4095)");
-        max_hh = std::max(max_hh, hh);
-        gate[(size_t)i] = make_int2(v->walk_period[i], v->walk_phase[i]);
-        attr[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
-    }
     const long long W = e->g.W;
     Ctl h{};
     h.tick = v->tick;
@@ -820,16 +895,8 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
             }
         }
     }
-    if (P > 0) {
-        SFC_CUDA(cudaMemcpyAsync(e->peds.center, v->center_xy, sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
-        SFC_CUDA(cudaMemcpyAsync(e->peds.gate, gate.data(), sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
-        SFC_CUDA(cudaMemcpyAsync(e->peds.attr, attr.data(), sizeof(uint32_t) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
-        SFC_CUDA(cudaMemsetAsync(e->peds.dir, 0xFF, (size_t)P, e->stream));
-        SFC_CUDA(cudaMemsetAsync(e->peds.moved_dir, 0xFF, (size_t)P, e->stream));
-        SFC_CUDA(cudaMemsetAsync(e->peds.won, 0, (size_t)P, e->stream));
-        SFC_CUDA(cudaMemsetAsync(e->peds.score, 0, sizeof(double) * (size_t)P, e->stream));
-        e->counters.h2d_bytes += (int64_t)((sizeof(int2) * 2 + sizeof(uint32_t)) * P);
-    }
+    rc = upload_peds(e, v, &gate, &attr, &max_hh);
+    if (rc != SFC_OK) return rc;
     if (e->slab.active) {
         // k-4 lists the two event cells of every mover for the next tick's clear: any pedestrian may move
         if (2 * P + 16 > e->slab.ev_capacity) {
@@ -846,45 +913,8 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
                                          "4*(pedestrian half-height+1) + density radius) rows)");
     }
     SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
-    if (e->marks_alloc.epoch) {
-        // The list pays when most tiles see no mover in a tick: a mover's field box overlaps about
-        // (w/32 + 1) x (h/8 + 1) tiles, every pedestrian may move.  Dense crowds skip the bookkeeping.
-        const TileMarks& m = e->marks_alloc;
-        const long long per_mover = (long long)((2 * m.hw + 1) / kMarkTileW + 2) * ((2 * m.hh + 1) / kMarkTileH + 2);
-        const long long n_tiles = (long long)m.tiles_x * m.tiles_y;
-        const bool sparse = P * per_mover < 2 * n_tiles; // (expected share of active tiles below ~85 %)
-        // Which k-5 formulation (all bit-identical; measured in profiles/README.md):
-        //   sparse crowd                 -> window kernel over the active-tile list (dense tiles: list walk / gather)
-        //   else, fields up to 11 x 11   -> the list-walk kernel alone: per-su cost fixed by the field area, at or
-        //                                   below the scatter kernel's from corridor densities up, far below for crowds
-        //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
-        //   fields beyond 15 x 15        -> the large-field kernel (every tile; sparse crowds: the window kernel)
-        const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || e->k5_path_pref < 0);
-        const int window = !pairs && e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
-        const int field = !pairs && !window && e->field.blob != nullptr &&
-                          (e->k5_path_pref == 4 || (e->k5_path_pref < 0 && e->walk.n > 224));
-        const int walk_only = !pairs && !window && !field && e->k5_listwalk &&
-                              (e->k5_path_pref == 2 || (e->k5_path_pref < 0 && e->walk.n <= 128));
-        if (e->k5_path_pref == 4 && !field && std::getenv("SFC_K5_STRICT"))
-            return fail(e, SFC_E_CONFIG, "SFC_K5_PATH=field: the large-field kernel does not support these tables / this shape");
-        const bool use = !field && (window || e->k5_active_list == 1 || (e->k5_active_list < 0 && sparse));
-        // the field kernel clears its partials per block unless the crowd is thin: expected events per field window
-        const double events_per_window = 2.0 * (double)P * (double)(e->walk.n + 1) / std::max(1.0, (double)e->g.W * (double)e->g.H);
-        const int lazy = field && (e->field_lazy_pref >= 0 ? e->field_lazy_pref : events_per_window < 24.0);
-        if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs ||
-            field != e->k5_field || lazy != e->field_lazy) {
-            e->marks = use ? m : TileMarks{};
-            e->k5_window = window;
-            e->k5_listwalk_only = walk_only;
-            e->k5_pairs = pairs;
-            e->k5_field = field;
-            e->field_lazy = lazy;
-            e->k5_launches = (walk_only || pairs || field) ? 1 : (window ? 2 : k5_kernels_per_launch(e->tabs, e->k5_event_max));
-            e->graph_valid = false;
-        }
-        // the tick counter may restart: forget every epoch stamp
-        SFC_CUDA(cudaMemsetAsync(m.epoch, 0, sizeof(unsigned) * (size_t)n_tiles, e->stream));
-    }
+    rc = select_k5_path(e, P, true);
+    if (rc != SFC_OK) return rc;
     if (!v->occupancy && P > 0) { // seed_population, scenario.cpp:424
         SFC_CUDA(launch_occupancy_from_peds(e->stream, e->g, e->peds, e->occ));
         e->counters.kernel_launches += 1;
@@ -1404,6 +1434,219 @@ int sfc_group_run(sfc_engine** engines, int n, int64_t ticks, sfc_tick_metrics* 
         }
     }
     return status;
+}
+
+// ---- band-swapped pass (state larger than device memory) --------------------------------------
+
+namespace {
+
+enum { kBandOcc = 1, kBandStat = 2, kBandDyn = 4, kBandEv = 8 };
+
+bool band_window(sfc_engine* e, int b) {
+    e->g.row0 = b * e->band_rows;
+    e->g.rows = std::min(e->band_rows, e->g.H - e->g.row0);
+    return e->g.rows > 0;
+}
+
+// Host -> device copy of the current window's rows (owned rows only, or owned + halo).  Rows beyond a
+// closed grid do not exist: occupancy "empty", no events there.
+int band_load(sfc_engine* e, const sfc_state_view* v, int what, bool owned_only) {
+    const long long W = e->g.W, C = (long long)(e->g.rows + 2 * e->g.halo) * W;
+    if (what & kBandOcc) SFC_CUDA(cudaMemsetAsync(e->occ, 0xFF, sizeof(int) * (size_t)C, e->stream));
+    if (what & kBandEv) SFC_CUDA(cudaMemsetAsync(e->ev, 0, (size_t)C * 2, e->stream));
+    for (const RowSeg& seg : row_segments(e, owned_only)) {
+        const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
+        if (what & kBandOcc) {
+            SFC_CUDA(bulk_copy(e, e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, true));
+            e->counters.h2d_bytes += (int64_t)(sizeof(int) * n_seg);
+        }
+        if (what & kBandEv) {
+            SFC_CUDA(bulk_copy(e, e->ev + 2 * dc, e->band_ev.data() + 2 * hc, (size_t)(2 * n_seg), true));
+            e->counters.h2d_bytes += (int64_t)(2 * n_seg);
+        }
+        if (what & kBandStat) {
+            SFC_CUDA(bulk_copy(e, e->stat + dc * kSects, v->static_image + hc * kSects, sizeof(float) * (size_t)n_seg * kSects, true));
+            e->counters.h2d_bytes += (int64_t)(sizeof(float) * n_seg * kSects);
+        }
+        if (what & kBandDyn) {
+            for (int k = 0; k < kKinds; ++k)
+                for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
+                    const long long n = std::min(e->stage_cells, n_seg - c0);
+                    SFC_CUDA(bulk_copy(e, e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects, true));
+                    SFC_CUDA(launch_interleave(e->stream, e->stage, e->dyn, k, dc + c0, n, e->ctl));
+                    e->counters.kernel_launches += 1;
+                    e->counters.h2d_bytes += (int64_t)(sizeof(float) * n * kSects);
+                }
+        }
+    }
+    return SFC_OK;
+}
+
+// Device -> host copy of the current window's rows (returns with the data on the host).
+int band_store(sfc_engine* e, sfc_state_view* v, int what, bool owned_only) {
+    const long long W = e->g.W;
+    for (const RowSeg& seg : row_segments(e, owned_only)) {
+        const long long hc = (long long)seg.global_row * W, dc = (long long)seg.local_row * W, n_seg = (long long)seg.rows * W;
+        if (what & kBandOcc) {
+            SFC_CUDA(bulk_copy(e, e->occ + dc, v->occupancy + hc, sizeof(int) * (size_t)n_seg, false));
+            e->counters.d2h_bytes += (int64_t)(sizeof(int) * n_seg);
+        }
+        if (what & kBandEv) {
+            SFC_CUDA(bulk_copy(e, e->ev + 2 * dc, e->band_ev.data() + 2 * hc, (size_t)(2 * n_seg), false));
+            e->counters.d2h_bytes += (int64_t)(2 * n_seg);
+        }
+        if (what & kBandDyn) {
+            for (int k = 0; k < kKinds; ++k)
+                for (long long c0 = 0; c0 < n_seg; c0 += e->stage_cells) {
+                    const long long n = std::min(e->stage_cells, n_seg - c0);
+                    SFC_CUDA(launch_deinterleave(e->stream, e->dyn, e->stage, k, dc + c0, n));
+                    SFC_CUDA(bulk_copy(e, e->stage, v->dyn_images[k] + (hc + c0) * kSects, sizeof(float) * (size_t)n * kSects, false));
+                    e->counters.kernel_launches += 1;
+                    e->counters.d2h_bytes += (int64_t)(sizeof(float) * n * kSects);
+                }
+        }
+    }
+    return SFC_OK;
+}
+
+} // namespace
+
+int sfc_band_plan(int32_t width, int32_t height, int32_t halo, int64_t n_peds, int64_t device_bytes, int device) {
+    if (device_bytes <= 0) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaSetDevice(device) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return -1;
+        device_bytes = (int64_t)(free_b - free_b / 16); // keep a margin for staging buffers and tables
+    }
+    const int64_t per_su = 4 + 32 + 96 + 2 + 1; // occupancy, static image, dynamic images, event map, k-5 work lists
+    const int64_t fixed = n_peds * 40 + (512ll << 20); // pedestrian arrays + staging
+    for (int bands = 1; bands <= height; ++bands) {
+        const int64_t rows = (height + bands - 1) / bands;
+        const int64_t resident = bands == 1 ? rows : rows + 2 * halo;
+        if (bands > 1 && (rows < halo || rows + 2 * halo > height)) return -1; // bands thinner than the halo: the state cannot be cut further
+        if (resident * width * per_su + fixed <= device_bytes) return bands;
+    }
+    return -1;
+}
+
+int sfc_band_run(sfc_engine* e, sfc_state_view* v, int64_t ticks, sfc_tick_metrics* metrics) {
+    if (e->band_count < 2) return fail(e, SFC_E_STATE, "band run on an engine created without bands");
+    if (!v->occupancy || !v->static_image || !v->dyn_images[0] || !v->dyn_images[1] || !v->dyn_images[2])
+        return fail(e, SFC_E_STATE, "band run: the host state must hold every dense array");
+    SFC_CUDA(cudaSetDevice(e->device));
+    const long long P = v->n_peds, W = e->g.W, H = e->g.H;
+    int rc = ensure_peds(e, P);
+    if (rc == SFC_OK) rc = ensure_stage(e);
+    if (rc == SFC_OK) rc = ensure_moved(e, std::max<int64_t>(ticks, 1));
+    if (rc != SFC_OK) return rc;
+    std::vector<int2> gate;
+    std::vector<uint32_t> attr;
+    int max_hh = 0;
+    Ctl h{};
+    h.tick = v->tick;
+    h.run_base = v->tick;
+    SFC_CUDA(cudaMemcpyAsync(e->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, e->stream));
+    rc = upload_peds(e, v, &gate, &attr, &max_hh);
+    if (rc != SFC_OK) return rc;
+    const int need = 4 * (max_hh + 1) + (e->dp.regulated ? e->dp.density_radius : 0);
+    if (e->g.halo < need || e->g.halo < e->tabs.max_hh)
+        return fail(e, SFC_E_CONFIG, "slab_halo: too shallow for this population (need max(field half-height, "
+                                     "4*(pedestrian half-height+1) + density radius) rows)");
+    e->ped_half_h = max_hh;
+    e->slab.reach = 0; // every pedestrian is resident: a band processes exactly the ones whose centre it owns
+    band_window(e, 0);
+    rc = select_k5_path(e, P, false);
+    if (rc != SFC_OK) return rc;
+    if (e->pairs_red) { // (float reductions need the upload-time subnormal scan of the whole images: plain read-modify-write here)
+        e->pairs_red = 0;
+    }
+    SFC_CUDA(cudaMemsetAsync(e->moved_counts, 0, sizeof(unsigned long long) * (size_t)std::max<int64_t>(ticks, 1), e->stream));
+    SFC_CUDA(cudaStreamSynchronize(e->stream)); // gate / attr staging vectors are consumed
+    e->band_ev.assign((size_t)(2 * W * H), 0);
+    e->tick = v->tick;
+    e->uploaded = true;
+    const DebugArrays none{};
+    const long long interval = e->cfg.rebuild_interval;
+    const int B = e->band_count;
+    int status = SFC_OK;
+    for (int64_t t = 0; t < ticks && status == SFC_OK; ++t) {
+        // pass A: k-2 — decisions (engine.cpp:341-363)
+        for (int b = 0; b < B && status == SFC_OK; ++b) {
+            if (!band_window(e, b)) break;
+            status = band_load(e, v, kBandOcc, false);
+            if (status == SFC_OK) status = band_load(e, v, kBandStat | kBandDyn, true);
+            if (status != SFC_OK) break;
+            SFC_CUDA(launch_k2_decide(e->stream, e->g, e->peds, e->occ, e->stat, e->dyn, e->ev, e->ctl, e->dp, e->slab));
+            e->counters.kernel_launches += 1;
+        }
+        // pass B: k-3 — votes (engine.cpp:365-386)
+        for (int b = 0; b < B && status == SFC_OK; ++b) {
+            if (!band_window(e, b)) break;
+            status = band_load(e, v, kBandOcc, false);
+            if (status != SFC_OK) break;
+            SFC_CUDA(launch_k3_vote(e->stream, e->g, e->peds, e->occ, e->ctl, e->dp, e->slab));
+            e->counters.kernel_launches += 1;
+        }
+        // pass C: k-4 — moves; occupancy and the tick's events go back band by band, halo rows included
+        if (status == SFC_OK) {
+            SFC_CUDA(cudaStreamSynchronize(e->stream));
+            std::fill(e->band_ev.begin(), e->band_ev.end(), (uint8_t)0);
+        }
+        for (int b = 0; b < B && status == SFC_OK; ++b) {
+            if (!band_window(e, b)) break;
+            status = band_load(e, v, kBandOcc | kBandEv, false);
+            if (status != SFC_OK) break;
+            SFC_CUDA(launch_k4_move(e->stream, e->g, e->peds, e->occ, e->ev, e->ctl, e->moved_counts, none, e->slab, TileMarks{}));
+            e->counters.kernel_launches += 1;
+            status = band_store(e, v, kBandOcc | kBandEv, false);
+        }
+        // pass D: k-5 — field write-back (engine.cpp:428-472)
+        for (int b = 0; b < B && status == SFC_OK; ++b) {
+            if (!band_window(e, b)) break;
+            status = band_load(e, v, kBandEv, false);
+            if (status == SFC_OK) status = band_load(e, v, kBandDyn, true);
+            if (status != SFC_OK) break;
+            SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 0)));
+            e->counters.kernel_launches += e->k5_launches;
+            status = band_store(e, v, kBandDyn, true);
+        }
+        if (status != SFC_OK) break;
+        SFC_CUDA(launch_tick_advance(e->stream, e->ctl));
+        e->counters.kernel_launches += 1;
+        e->tick += 1;
+        if (interval > 0 && e->tick % interval == 0) { // maybe_rebuild (engine.cpp:538-550): check every band, then commit every band
+            for (int pass = 1; pass <= 2 && status == SFC_OK; ++pass) {
+                for (int b = 0; b < B && status == SFC_OK; ++b) {
+                    if (!band_window(e, b)) break;
+                    status = band_load(e, v, kBandOcc, false);
+                    if (status == SFC_OK) status = band_load(e, v, kBandDyn, true);
+                    if (status != SFC_OK) break;
+                    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, pass, 0.0));
+                    e->counters.kernel_launches += 1;
+                    if (pass == 2) status = band_store(e, v, kBandDyn, true);
+                }
+                if (pass == 1 && status == SFC_OK) {
+                    SFC_CUDA(launch_drift_verdict(e->stream, e->ctl, e->cfg.rebuild_tolerance));
+                    e->counters.kernel_launches += 1;
+                }
+            }
+        }
+    }
+    band_window(e, 0);
+    if (status != SFC_OK) return status;
+    std::vector<unsigned long long> moved((size_t)std::max<int64_t>(ticks, 0));
+    if (ticks > 0)
+        SFC_CUDA(cudaMemcpyAsync(moved.data(), e->moved_counts, sizeof(unsigned long long) * (size_t)ticks, cudaMemcpyDeviceToHost, e->stream));
+    if (P > 0 && v->center_xy)
+        SFC_CUDA(cudaMemcpyAsync(v->center_xy, e->peds.center, sizeof(int2) * (size_t)P, cudaMemcpyDeviceToHost, e->stream));
+    rc = check_device_error(e); // synchronises; refreshes e->tick
+    v->tick = e->tick;
+    if (metrics)
+        for (int64_t t = 0; t < ticks; ++t) {
+            metrics[t] = sfc_tick_metrics{};
+            metrics[t].tick = h.tick + t;
+            metrics[t].moved = (int64_t)moved[(size_t)t];
+        }
+    return rc;
 }
 
 int sfc_digest(sfc_engine* e, uint64_t* digest) {

@@ -78,6 +78,8 @@ struct SlabDev {
     int reach;                // k-3 / k-4 also run for neighbours' pedestrians this many rows beyond the edge
     long long* ev_written;    // event-map cells written this tick (cleared at the start of the next)
     long long ev_capacity;
+    int band;                 // band-swapped engine: every pedestrian is resident and processed by the band that owns
+                              // its centre NOW — k-4 retires its vote flag so a mover is not moved again by the next band
 };
 
 // sect_step (fields.cpp:67-72) without a table: sect 0 = +x, counter-clockwise.

@@ -348,7 +348,9 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             if (to >= 0) ev[2 * to + 1] = code;
             p.moved_dir[i] = (int8_t)d;
             if (marks.epoch) mark_tiles(g, marks, ctl, ctl->epoch, c.x, c.y, ux, uy, slab.active != 0);
-            if (slab.active) { // remember the event cells for next tick's clear
+            if (slab.band) {
+                p.won[i] = 0;
+            } else if (slab.active) { // remember the event cells for next tick's clear
                 const int at = atomicAdd(&ctl->ev_written_count, 2);
                 if (at + 1 < slab.ev_capacity) {
                     slab.ev_written[at] = from >= 0 ? 2 * from : -1;

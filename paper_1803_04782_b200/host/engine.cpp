@@ -223,6 +223,8 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
     if (cfg_.workers <= 0) cfg_.workers = 1; // no host workers exist; keep the field well-formed
     if (const char* knob = std::getenv("SFC_SLABS")) cfg_.slabs = std::atoi(knob); // test hook: force a slab group
     if (cfg_.slabs < 1) throw ConfigError("slabs", "must be >= 1");
+    if (const char* knob = std::getenv("SFC_BANDS")) cfg_.bands = std::atoi(knob); // test hook: force a band-swapped run
+    if (cfg_.bands < 0) throw ConfigError("bands", "must be >= 0 (0 = as many as the device memory requires)");
 
     std::array<bridge::KindTable, kDynKinds> tables;
     for (int k = 0; k < kDynKinds; ++k) {
@@ -240,7 +242,9 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
         }
         tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(spec);
     }
-    dev_ = bridge::create_engine(geom_, cfg_, tables);
+    // A banded configuration may describe a state larger than the device's memory: the whole-grid
+    // engine is then only built when something other than run() needs it (require_device).
+    if (cfg_.bands == 1) dev_ = bridge::create_engine(geom_, cfg_, tables);
 
     const std::size_t cells = static_cast<std::size_t>(geom_.cells());
     enrollment_.reset_geometry(geom_);
@@ -251,7 +255,78 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
 
 Engine::~Engine() {
     release_slabs();
-    sfc_destroy(dev_);
+    if (band_engine_) sfc_destroy(band_engine_);
+    if (dev_) sfc_destroy(dev_);
+}
+
+void Engine::require_device() const {
+    if (dev_) return;
+    std::array<bridge::KindTable, kDynKinds> tables;
+    for (int k = 0; k < kDynKinds; ++k) tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(field_templates_[static_cast<std::size_t>(k)]);
+    const_cast<Engine*>(this)->dev_ = bridge::create_engine(geom_, cfg_, tables);
+}
+
+// run() for a state that does not fit the device: the caller's host SimState is the backing store and
+// the SU grid streams through the device in row bands, one phase at a time (sfc_band_run).
+std::vector<TickMetrics> Engine::run_bands(SimState& s, long ticks, int bands) {
+    int ped_half_h = 0, field_half_h = 0;
+    for (const Pedestrian& p : s.pedestrians) ped_half_h = std::max(ped_half_h, p.footprint.half_h());
+    for (const FieldSpec& f : field_templates_) field_half_h = std::max(field_half_h, f.geometry.half_h());
+    const int halo = sfc_slab_halo_rows(field_half_h, ped_half_h,
+                                        cfg_.regulation == Regulation::Linear ? cfg_.density_radius : 0);
+    if (bands <= 0) {
+        std::int64_t budget = 0; // 0: what the device reports free
+        if (const char* knob = std::getenv("SFC_BAND_DEVICE_BYTES")) budget = std::atoll(knob); // plan against a smaller device
+        bands = sfc_band_plan(geom_.width, geom_.height, halo, static_cast<std::int64_t>(s.pedestrians.size()), budget, cfg_.device);
+        if (bands < 1) throw ConfigError("bands", "the state does not fit the device even in bands one halo tall");
+        if (bands == 1) { // it fits: the ordinary resident path
+            require_device();
+            upload(s);
+            std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
+            const int status = sfc_run(dev_, ticks, raw.data(), 0);
+            download(s);
+            if (status != SFC_OK) throw_status(status);
+            std::vector<TickMetrics> metrics;
+            for (const auto& r : raw) metrics.push_back(to_metrics(r));
+            return metrics;
+        }
+    }
+    if (bands < 2) throw ConfigError("bands", "a band-swapped run needs at least 2 bands");
+    const int rows = (geom_.height + bands - 1) / bands;
+    if (!band_engine_ || band_engine_bands_ != bands || slab_halo_ != halo) {
+        if (band_engine_) sfc_destroy(band_engine_);
+        band_engine_ = nullptr;
+        std::array<bridge::KindTable, kDynKinds> tables;
+        for (int k = 0; k < kDynKinds; ++k) tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(field_templates_[static_cast<std::size_t>(k)]);
+        sfc_tables t{};
+        for (int k = 0; k < kDynKinds; ++k) t.kind[k] = tables[static_cast<std::size_t>(k)].view();
+        sfc_config c = bridge::make_config(geom_, cfg_);
+        c.slab_row0 = 0;
+        c.slab_rows = rows;
+        c.slab_halo = halo;
+        c.bands = (geom_.height + rows - 1) / rows;
+        char why[512] = {0};
+        const int status = sfc_create(&c, &t, &band_engine_, why, sizeof why);
+        if (status != SFC_OK) bridge::throw_status(status, why, s.tick, 0);
+        band_engine_bands_ = bands;
+        slab_halo_ = halo;
+    }
+    bridge::PedColumns cols;
+    sfc_state_view v = make_view(s, cols);
+    std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
+    const int status = sfc_band_run(band_engine_, &v, ticks, raw.data());
+    for (std::size_t i = 0; i < s.pedestrians.size(); ++i) s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
+    s.tick = static_cast<long>(v.tick);
+    if (status != SFC_OK) {
+        std::int64_t tick = -1;
+        std::int32_t phase = 0;
+        sfc_error_detail(band_engine_, &tick, &phase, nullptr, nullptr, nullptr);
+        bridge::throw_status(status, sfc_last_error(band_engine_), static_cast<long>(tick), phase);
+    }
+    std::vector<TickMetrics> metrics;
+    metrics.reserve(raw.size());
+    for (const auto& r : raw) metrics.push_back(to_metrics(r));
+    return metrics;
 }
 
 void Engine::release_slabs() {
@@ -335,6 +410,7 @@ void Engine::throw_status(int status) const {
 }
 
 void Engine::upload(const SimState& s) {
+    require_device();
     require_shape(s, geom_);
     bridge::PedColumns cols;
     const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);
@@ -344,6 +420,7 @@ void Engine::upload(const SimState& s) {
 }
 
 void Engine::download(SimState& s) {
+    require_device();
     bridge::PedColumns cols;
     sfc_state_view v = make_view(s, cols);
     v.static_image = nullptr; // a tick never writes it
@@ -374,6 +451,7 @@ sfc_state_view population_view(const std::vector<Pedestrian>& peds, long tick, b
 } // namespace
 
 void Engine::seed_resident(const std::vector<Pedestrian>& pedestrians, long tick) {
+    require_device();
     bridge::PedColumns cols;
     const sfc_state_view v = population_view(pedestrians, tick, cols);
     const int status = sfc_upload(dev_, &v);
@@ -382,6 +460,7 @@ void Engine::seed_resident(const std::vector<Pedestrian>& pedestrians, long tick
 }
 
 std::vector<SuIndex> Engine::download_centers() {
+    require_device();
     std::vector<std::int32_t> xy(2 * decisions_.size());
     sfc_state_view v{};
     v.n_peds = static_cast<std::int64_t>(decisions_.size());
@@ -394,10 +473,12 @@ std::vector<SuIndex> Engine::download_centers() {
 }
 
 void Engine::set_static_resident(const std::vector<AnchoredField>& fields) {
+    require_device();
     bridge::rasterize_static_on(dev_, fields);
 }
 
 std::uint64_t Engine::digest_resident() {
+    require_device();
     std::uint64_t h = 0;
     const int status = sfc_digest(dev_, &h);
     if (status != SFC_OK) throw_status(status);
@@ -406,6 +487,8 @@ std::uint64_t Engine::digest_resident() {
 
 bool Engine::resident_identical(Engine& other, std::string* diagnosis) { // wording of states_identical, engine.cpp:103-156
     sfc_difference d{};
+    require_device();
+    other.require_device();
     const int status = sfc_compare(dev_, other.dev_, &d);
     if (status != SFC_OK) throw_status(status);
     if (d.what == 0) return true;
@@ -426,6 +509,7 @@ bool Engine::resident_identical(Engine& other, std::string* diagnosis) { // word
 }
 
 std::vector<TickMetrics> Engine::step_resident(long ticks, bool phase_times) {
+    require_device();
     std::vector<TickMetrics> out;
     if (ticks <= 0) return out;
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
@@ -437,6 +521,7 @@ std::vector<TickMetrics> Engine::step_resident(long ticks, bool phase_times) {
 }
 
 void Engine::pull_temporaries(int phase, SimState& s) {
+    require_device();
     const std::size_t cells = static_cast<std::size_t>(geom_.cells());
     std::vector<std::uint8_t> from(3 * cells), to(3 * cells);
     std::vector<std::int32_t> dirs(s.pedestrians.size());
@@ -468,6 +553,7 @@ void Engine::pull_temporaries(int phase, SimState& s) {
 TickMetrics Engine::tick(SimState& s, RunMode mode) { return tick(s, mode, Inspector{}); }
 
 TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect) {
+    require_device();
     upload(s);
     TickMetrics m;
     m.tick = s.tick;
@@ -509,6 +595,7 @@ std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, cons
         return metrics;
     }
     if (cfg_.slabs > 1) return run_slabs(s, ticks);
+    if (cfg_.bands != 1) return run_bands(s, ticks, cfg_.bands);
     upload(s);
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
     const int status = sfc_run(dev_, ticks, raw.data(), 0);
@@ -520,6 +607,7 @@ std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, cons
 }
 
 MoveDecision Engine::decide(const Pedestrian& p, const SimState& s) const {
+    require_device();
     require_shape(s, geom_);
     // The device decides for the pedestrian stored at p.id; substitute `p` there so callers may
     // probe a modified copy, as the reference's by-value semantics allow.
@@ -541,6 +629,7 @@ MoveDecision Engine::decide(const Pedestrian& p, const SimState& s) const {
 }
 
 std::array<StrengthImage, kDynKinds> Engine::rebuild_images(const SimState& s) const {
+    require_device();
     require_shape(s, geom_);
     bridge::PedColumns cols;
     const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);

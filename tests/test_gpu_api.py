@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle, shim
+from tests import scenarios as sc
 from paper_1803_04782_b200 import socfield as sf
 
 pytestmark = pytest.mark.gpu
@@ -458,3 +459,41 @@ def test_one_run_across_the_stamp_period(monkeypatch):
     assert [m.moved for m in ma[-200:]] == [m.moved for m in mb[-200:]]
     same, why = sf.states_identical(a_state, b_state)
     assert same, why
+
+
+@pytest.mark.parametrize("name,bands", [("desk64", 2), ("desk64", 3), ("closed-four", 2), ("linear-regulation", 2), ("wide-ragged", 3),
+                                        ("field21", 2), ("ped5", 2), ("k16", 2), ("field35", 2), ("d0.9-eight-ped1", 4)])
+def test_band_swapped_pass_equals_undivided_grid(product_lib, monkeypatch, name, bands):
+    """A state larger than device memory streams through the device in row bands, the host SimState
+    being the backing store (sfc_band_run: the paper's divide-and-conquer as a band pass; reference
+    accumulator.hpp:68-83, bench.cpp:14-24).  Forced here on small grids with SFC_BANDS: bit-identical
+    to the oracle — i.e. to the undivided grid — across rebuilds, for every k-5 kernel family."""
+    monkeypatch.setenv("SFC_BANDS", str(bands))
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for chunk in (1, 7, 14):
+        np.testing.assert_array_equal(gpu.run(chunk), cpu.run(chunk), err_msg=f"{name} x{bands} moved")
+        assert gpu.tick == cpu.tick
+        np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"{name} x{bands} tick {gpu.tick} centres")
+        np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"{name} x{bands} tick {gpu.tick} occupancy")
+        for k in range(3):
+            np.testing.assert_array_equal(gpu.image(k).view(np.uint32), cpu.image(k).view(np.uint32), err_msg=f"{name} x{bands} image {k}")
+    gpu.verify()
+
+
+def test_band_plan_counts_bands_from_device_memory():
+    """sfc_band_plan: 1 band when the state fits, more as the budget shrinks, -1 when a band cannot be cut thinner
+    than its halo (134 B per resident su)."""
+    import ctypes
+
+    from paper_1803_04782_b200 import build
+
+    lib = ctypes.CDLL(build.build_all(force=False, verbose=False)["cuda"])
+    lib.sfc_band_plan.restype = ctypes.c_int
+    lib.sfc_band_plan.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
+    state = 135 * 49152 * 49152  # a 49152^2 grid: 326 GB resident, beyond one B200
+    assert lib.sfc_band_plan(49152, 49152, 4, 1_000_000, 2 * state, 0) == 1
+    assert lib.sfc_band_plan(49152, 49152, 4, 1_000_000, 170 << 30, 0) == 2
+    assert lib.sfc_band_plan(49152, 49152, 4, 1_000_000, 60 << 30, 0) == 6
+    assert lib.sfc_band_plan(64, 64, 40, 100, 1 << 20, 0) == -1
