@@ -30,7 +30,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 
 CUDA_SOURCES = ["sfc_api.cu", "sfc_ped_kernels.cu", "sfc_k5_writeback.cu", "sfc_k5_window.cu", "sfc_k5_listwalk.cu", "sfc_k5_pairs.cu", "sfc_k5_field.cu", "sfc_rasterize.cu", "sfc_slab.cu", "sfc_digest.cu"]
-HOST_SOURCES = ["model.cpp", "engine.cpp", "raster.cpp", "scenario.cpp"]
+HOST_SOURCES = ["model.cpp", "engine.cpp", "raster.cpp", "scenario.cpp", "bench.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

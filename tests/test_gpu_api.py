@@ -497,3 +497,35 @@ def test_band_plan_counts_bands_from_device_memory():
     assert lib.sfc_band_plan(49152, 49152, 4, 1_000_000, 170 << 30, 0) == 2
     assert lib.sfc_band_plan(49152, 49152, 4, 1_000_000, 60 << 30, 0) == 6
     assert lib.sfc_band_plan(64, 64, 40, 100, 1 << 20, 0) == -1
+
+
+def test_run_bench_sweeps_like_the_reference():
+    """run_bench on the CUDA engine (reference bench.cpp:65-124; cases of test_bench_cli.cpp:69-141):
+    cross-product row counting, a failing combination recorded while the sweep continues, one row
+    per walk period, exclusive axes; the report keeps the reference's header and columns."""
+    base = sf.parse_scenario("grid = 16x16\ndensity = 0.3\n")
+    rows, csv = sf.run_bench(base, grids=[(12, 12), (16, 16)], densities=[0.2, 0.4], directions=["uni"], ticks=2, repeats=2,
+                             warmup=False, gpu_columns=False)
+    assert len(rows) == 4
+    for r in rows:
+        assert r["status"] == "ok" and r["repeats"] == 2 and r["min_ms"] <= r["mean_ms"] <= r["max_ms"] and r["device_mean_ms"] > 0
+    lines = csv.strip().splitlines()
+    assert len(lines) == 5
+    assert lines[0] == ("grid,density,directions,field_geometry,pedestrian_geometry,walk_period_max,population,sf,ticks,repeats,"
+                        "mean_ms,min_ms,max_ms,status")
+    assert [r["grid"] for r in rows] == [(12, 12), (12, 12), (16, 16), (16, 16)] and [r["density"] for r in rows] == [0.2, 0.4, 0.2, 0.4]
+
+    base = sf.parse_scenario("grid = 10x10\n")
+    rows, _ = sf.run_bench(base, densities=[0.9, 0.3], pedestrian_geometries=[(3, 3)], ticks=1, repeats=1, warmup=False)
+    assert len(rows) == 2 and rows[0]["status"].startswith("error:") and rows[1]["status"] == "ok"
+    assert rows[1]["field_geometry"] == (21, 21)  # joint geometry: fields scale with the body
+
+    base = sf.parse_scenario("grid = 12x12\ndensity = 0.4\n")
+    rows, csv = sf.run_bench(base, walk_period_maxes=[1, 3, 5, 7, 9, 11], ticks=1, repeats=1, warmup=False)
+    assert [r["walk_period_max"] for r in rows] == [1, 3, 5, 7, 9, 11] and all(r["status"] == "ok" for r in rows)
+    assert csv.splitlines()[0].endswith("device_mean_ms,ped_steps_per_s,su_updates_per_s,status")
+
+    with pytest.raises(sf.ConfigError):
+        sf.run_bench(base, field_ratios=[1], pedestrian_geometries=[(1, 1)])
+    rows, _ = sf.run_bench(base, field_ratios=[1, 3], ticks=1, repeats=1, warmup=False)
+    assert [r["field_geometry"] for r in rows] == [(7, 7), (21, 21)] and [r["sf"] for r in rows] == [7, 64]

@@ -48,7 +48,7 @@ def test_python_surface_matches_reference_module():
                  "chunk_count", "sort8_desc", "ScenarioConfig", "parse_scenario", "parse_scenario_file",
                  "serialize_scenario", "validate_scenario", "planned_population", "scale_fields", "SimState",
                  "seed_population", "states_identical", "TickMetrics", "Engine", "ParseError", "ConfigError",
-                 "SeedingError", "IntegrityError"]:
+                 "SeedingError", "IntegrityError", "MemoryPlan", "memory_plan"]:
         assert hasattr(sf, name), name
     for method in ["tick", "run", "verify_state", "plan_fanout"]:
         assert hasattr(sf.Engine, method)
@@ -173,3 +173,21 @@ def test_strength_law_equals_oracle():
                 sx, sy = C.c_double(), C.c_double()
                 L.so_strength_at_offset(kind_i, C.byref(of), 5, dx, dy, C.byref(sx), C.byref(sy))
                 assert sf.strength_at(f, (20, 20), (20 + dx, 20 + dy), grid) == (sx.value, sy.value)
+
+
+def test_memory_plan_numbers_and_errors():
+    """memory_plan (reference bench.cpp:14-24): paper section 3.2's one-step cache arithmetic — the
+    reference's own cases (test_bench_cli.cpp:41-67, tests/python/test_smoke.py:9-15)."""
+    grid = sf.GridGeometry(1000, 1000)
+    for fanout, m_recur, gib in [(6, 192, 0.7), (61, 1952, 7.3), (164, 5248, 19.6), (328, 10496, 39.1), (535, 17120, 63.8),
+                                 (808, 25856, 96.3)]:
+        plan = sf.memory_plan(fanout, grid)
+        assert plan.sf == fanout and plan.m_recur_bytes == m_recur and plan.m_total_bytes == 4 * m_recur
+        assert plan.grid_bytes == plan.m_total_bytes * 1_000_000
+        assert abs(plan.gib_display - gib) <= 0.05
+    zero = sf.memory_plan(0, grid)
+    assert (zero.m_recur_bytes, zero.m_total_bytes, zero.grid_bytes, zero.gib) == (0, 0, 0, 0.0)
+    with pytest.raises(sf.ConfigError):
+        sf.memory_plan(-1, sf.GridGeometry(10, 10))
+    # BASELINE config 3 (35 x 35 fields: fan-out 179 on 8192^2): the one-step cache would need 1432 GiB
+    assert round(sf.memory_plan(179, sf.GridGeometry(8192, 8192)).gib) == 1432
