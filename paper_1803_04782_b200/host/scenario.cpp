@@ -308,7 +308,9 @@ std::vector<SuIndex> draw_centres(const ScenarioConfig& cfg, std::int64_t want, 
     const int rw = body.half_w(), rh = body.half_h();
     std::vector<SuIndex> centres;
     centres.reserve(static_cast<std::size_t>(want));
-    OccupancyGrid taken(g);
+    // one bit per su (the reference keeps a 4-byte OccupancyGrid here: 4.3 GB at 32768^2, 134 MB as bits)
+    std::vector<std::uint64_t> taken((static_cast<std::size_t>(g.cells()) + 63) / 64, 0);
+    const auto bit_of = [&g](SuIndex su) { return static_cast<std::size_t>(su.y) * static_cast<std::size_t>(g.width) + static_cast<std::size_t>(su.x); };
     std::uniform_int_distribution<int> pick_x(0, g.width - 1);
     std::uniform_int_distribution<int> pick_y(0, g.height - 1);
 
@@ -318,7 +320,10 @@ std::vector<SuIndex> draw_centres(const ScenarioConfig& cfg, std::int64_t want, 
             return false;
         const FootprintCells cells = footprint_cells(g, c, body);
         if (cells.clipped) return false;
-        return std::all_of(cells.cells.begin(), cells.cells.end(), [&](SuIndex su) { return taken.empty_at(su); });
+        return std::all_of(cells.cells.begin(), cells.cells.end(), [&](SuIndex su) {
+            const std::size_t b = bit_of(su);
+            return ((taken[b >> 6] >> (b & 63)) & 1u) == 0;
+        });
     };
 
     std::int64_t draws_left = 64 * want;
@@ -333,7 +338,10 @@ std::vector<SuIndex> draw_centres(const ScenarioConfig& cfg, std::int64_t want, 
             const int y = pick_y(rng);
             const SuIndex c{x, y};
             if (!fits(c)) continue;
-            for (const SuIndex su : footprint_cells(g, c, body).cells) taken.set(su, static_cast<std::int32_t>(centres.size()));
+            for (const SuIndex su : footprint_cells(g, c, body).cells) {
+                const std::size_t b = bit_of(su);
+                taken[b >> 6] |= std::uint64_t{1} << (b & 63);
+            }
             centres.push_back(c);
             break;
         }

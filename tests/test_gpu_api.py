@@ -529,3 +529,28 @@ def test_run_bench_sweeps_like_the_reference():
         sf.run_bench(base, field_ratios=[1], pedestrian_geometries=[(1, 1)])
     rows, _ = sf.run_bench(base, field_ratios=[1, 3], ticks=1, repeats=1, warmup=False)
     assert [r["field_geometry"] for r in rows] == [(7, 7), (21, 21)] and [r["sf"] for r in rows] == [7, 64]
+
+
+def test_validate_tool_exit_codes(tmp_path, capsys):
+    """`validate` (reference cmd_validate, cli.cpp:79-140; cases of test_bench_cli.cpp:175-198): two execution
+    strategies of the engine in lockstep, compared on the device — identical runs exit 0, the injected vote
+    tie-break fault is caught (exit 4), a malformed scenario exits 1, an impossible one 2."""
+    from paper_1803_04782_b200 import validate
+
+    desk = tmp_path / "desk.scn"
+    desk.write_text(sc.variant(sc.DESK64, ticks=12))
+    assert validate.main([str(desk)]) == 0
+    assert validate.main([str(desk), "--variant", "SFC_K5_PATH=scatter,SFC_K5_EVENT_MAX=3"]) == 0
+    assert validate.main([str(desk), "--variant", "SFC_K5_PATH=field", "--every", "4"]) == 0
+    assert validate.main([str(desk), "--slabs", "2", "--every", "6"]) == 0
+    assert validate.main([str(desk), "--bands", "2", "--every", "6"]) == 0
+    assert "identical over 12 ticks" in capsys.readouterr().out
+    assert validate.main([str(desk), "--ticks", "40", "--inject-tiebreak-fault"]) == 4
+    assert "divergence at tick" in capsys.readouterr().err
+    bad = tmp_path / "bad.scn"
+    bad.write_text("grid = banana\n")
+    assert validate.main([str(bad)]) == 1
+    dense = tmp_path / "dense.scn"
+    dense.write_text("grid = 10x10\ndensity = 1.5\n")
+    assert validate.main([str(dense)]) == 2
+    assert validate.main([str(tmp_path / "absent.scn")]) == 1
