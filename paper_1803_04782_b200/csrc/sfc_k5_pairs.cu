@@ -123,27 +123,55 @@ __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArg
     const uint16_t* const ev16 = reinterpret_cast<const uint16_t*>(a.ev);
     const bool listed = a.marks.epoch != nullptr;
     const int n_edge = listed ? tile_edge_count(a.marks) : 0;
-    const long long n_items = 8ll * (listed ? n_edge + a.ctl->active_count : a.n_tiles);
+    const long long n_tiles_todo = listed ? (long long)n_edge + a.ctl->active_count : 8ll * a.n_tiles; // (unlisted: items are blocks)
     const long long stride = (long long)gridDim.x * kWarps;
     const int sx = lane & 7, sy = lane >> 3;
     const int c = lane & 15, r0 = lane >> 4; // staging: lanes 0-15 the even region row of a pass, 16-31 the odd one
 
-    // Finds the next block at or after `item` that can hold work (a listed tile's block within some
-    // mover's reach, inside the grid) and issues the loads of its region: two region rows per pass.
-    long long item = (long long)blockIdx.x * kWarps + warp;
+    // With the active-tile list, work items are TILES (a warp takes every stride-th one) and, within a tile,
+    // the blocks some mover's field box touches (the stamp's block bits).  The tile id and stamp of the NEXT tile are loaded while
+    // this tile's blocks are processed: the list -> stamp -> region chain of dependent loads is paid once
+    // per tile, overlapped, not once per block.
+    long long tile_item = (long long)blockIdx.x * kWarps + warp;
+    auto tile_of = [&](long long t, uint32_t& mask) -> int { // tile id and its live-block mask
+        mask = 0xFFu;
+        if (t < n_edge) { // slab mode: tiles whose region reaches the halo rows are always processed
+            const int r = (int)t / a.tiles_x;
+            const int ty = r < a.marks.edge_lo ? r : a.marks.edge_hi + (r - a.marks.edge_lo);
+            return ty * a.tiles_x + ((int)t - r * a.tiles_x);
+        }
+        const int tile = a.marks.list[t - n_edge];
+        mask = (a.marks.epoch[tile] >> 8) & 0xFFu; // blocks within reach of a mover
+        return tile;
+    };
+    int cur_tile = 0, pre_tile = 0;
+    uint32_t cur_mask = 0u, pre_mask = 0u;
+    bool pre_valid = listed && tile_item < n_tiles_todo;
+    if (pre_valid) pre_tile = tile_of(tile_item, pre_mask);
+
+    // Finds the next block that can hold work (inside the grid) and issues the loads of its region: two
+    // region rows per pass.
     auto fetch = [&](int& x0, int& y0, uint32_t (&code)[PASSES]) -> bool {
-        for (; item < n_items; item += stride) {
-            const int t = (int)(item >> 3), b = (int)(item & 7);
-            int tile;
-            if (!listed) {
-                tile = t;
-            } else if (t < n_edge) { // slab mode: tiles whose region reaches the halo rows are always processed
-                const int r = t / a.tiles_x;
-                const int ty = r < a.marks.edge_lo ? r : a.marks.edge_hi + (r - a.marks.edge_lo);
-                tile = ty * a.tiles_x + (t - r * a.tiles_x);
+        for (;;) {
+            int b, tile;
+            if (!listed) { // every block of every tile: spread block by block over the warps of the grid
+                if (tile_item >= n_tiles_todo) return false;
+                tile = (int)(tile_item >> 3);
+                b = (int)(tile_item & 7);
+                tile_item += stride;
             } else {
-                tile = a.marks.list[t - n_edge];
-                if (!((a.marks.epoch[tile] >> (8 + b)) & 1u)) continue; // no mover's field box touches this block
+                if (cur_mask == 0u) { // next tile: adopt the prefetched one, start the prefetch of the one after
+                    if (!pre_valid) return false;
+                    cur_tile = pre_tile;
+                    cur_mask = pre_mask;
+                    tile_item += stride;
+                    pre_valid = tile_item < n_tiles_todo;
+                    if (pre_valid) pre_tile = tile_of(tile_item, pre_mask);
+                    continue;
+                }
+                b = __ffs((int)cur_mask) - 1;
+                cur_mask &= cur_mask - 1u;
+                tile = cur_tile;
             }
             int tile_y = (int)__umulhi((unsigned)tile, a.inv_tiles_x), tile_x = tile - tile_y * a.tiles_x;
             if (tile_x >= a.tiles_x) {
@@ -172,10 +200,8 @@ __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArg
                     code[p] = idx >= 0 ? __ldg(ev16 + idx) : 0u;
                 }
             }
-            item += stride;
             return true;
         }
-        return false;
     };
 
     // image += (float)total is a read-modify-write of a value nobody else touches: the load is
