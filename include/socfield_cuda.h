@@ -187,6 +187,12 @@ int sfc_reset_dynamic_images(sfc_engine* e);
 int sfc_rasterize_static(sfc_engine* e, int32_t n_tables, const sfc_kind_table* tables, int64_t n_anchors,
                          const sfc_anchor* anchors, const float* base, float* out);
 
+/* Page-lock / unlock a host array the caller hands to sfc_upload / sfc_download again and again
+ * (cudaHostRegister): copies from a locked array are single DMAs at PCIe rate, the copy path detects the
+ * lock by itself.  Returns 0 on success; failure only means the staged copy path is used. */
+int sfc_host_pin(const void* ptr, size_t bytes);
+int sfc_host_unpin(const void* ptr);
+
 /* ---- Row slabs across GPUs (no counterpart in the reference, which is single address space;
  * SURVEY.md 8e).  An engine created with sfc_config.slab_rows < height owns rows
  * [slab_row0, slab_row0 + slab_rows) and keeps slab_halo more rows resident on each side.

@@ -249,7 +249,13 @@ void stager_destroy(sfc_engine* e) {
 // the engine's stream.  to_device: the host buffer may be reused on return and later work on the
 // engine's stream sees the data.  Otherwise the host buffer holds the data on return.
 cudaError_t bulk_copy(sfc_engine* e, void* dev, void* host, size_t bytes, bool to_device) {
-    if (bytes < (1u << 20) || !stager_init(e)) {
+    bool locked = false;
+    if (bytes >= (1u << 20)) { // page-locked by its owner (sfc_host_pin): one DMA, no staging
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, host) == cudaSuccess) locked = attr.type == cudaMemoryTypeHost;
+        else cudaGetLastError();
+    }
+    if (locked || bytes < (1u << 20) || !stager_init(e)) {
         cudaError_t c = to_device ? cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, e->stream)
                                   : cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, e->stream);
         if (c == cudaSuccess && !to_device) c = cudaStreamSynchronize(e->stream);
@@ -1315,6 +1321,26 @@ int sfc_slab_buffer(sfc_engine* e, int kind, int edge, int recv, void** ptr, siz
 }
 
 void* sfc_stream(sfc_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
+int sfc_host_pin(const void* ptr, size_t bytes) {
+    if (!ptr || bytes == 0) return -1;
+    const cudaError_t c = cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterPortable);
+    if (c != cudaSuccess) {
+        cudaGetLastError(); // (not sticky; the caller falls back to the staged copy)
+        return -1;
+    }
+    return 0;
+}
+
+int sfc_host_unpin(const void* ptr) {
+    if (!ptr) return -1;
+    const cudaError_t c = cudaHostUnregister(const_cast<void*>(ptr));
+    if (c != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return 0;
+}
 
 int sfc_slab_finish(sfc_engine* e, int64_t first_tick, int64_t ticks, int64_t* moved) {
     SFC_CUDA(cudaSetDevice(e->device));

@@ -5,7 +5,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <sstream>
+#include <thread>
 
 #include "device_bridge.hpp"
 
@@ -158,6 +160,10 @@ sfc_state_view make_view(SimState& s, bridge::PedColumns& cols) { return bridge:
 
 sfc_state_view bridge::view_of(SimState& s, PedColumns& cols) {
     cols.gather(s.pedestrians);
+    // the dense arrays cross PCIe on every run: page-lock them once, for as long as their storage lives
+    s.occupancy.pin();
+    s.static_image.pin();
+    for (const StrengthImage& img : s.dyn_images) img.pin();
     sfc_state_view v{};
     v.tick = s.tick;
     v.n_peds = static_cast<std::int64_t>(s.pedestrians.size());
@@ -586,17 +592,37 @@ TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect
 std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode) { return run(s, ticks, mode, Inspector{}); }
 
 std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, const Inspector& inspect) {
-    verify_state(s);
     std::vector<TickMetrics> metrics;
-    if (ticks <= 0) return metrics;
-    if (inspect) {
-        metrics.reserve(static_cast<std::size_t>(ticks));
-        for (long i = 0; i < ticks; ++i) metrics.push_back(tick(s, mode, inspect));
-        return metrics;
+    if (ticks <= 0 || inspect || cfg_.slabs > 1 || cfg_.bands != 1) {
+        verify_state(s);
+        if (ticks <= 0) return metrics;
+        if (inspect) {
+            metrics.reserve(static_cast<std::size_t>(ticks));
+            for (long i = 0; i < ticks; ++i) metrics.push_back(tick(s, mode, inspect));
+            return metrics;
+        }
+        if (cfg_.slabs > 1) return run_slabs(s, ticks);
+        return run_bands(s, ticks, cfg_.bands);
     }
-    if (cfg_.slabs > 1) return run_slabs(s, ticks);
-    if (cfg_.bands != 1) return run_bands(s, ticks, cfg_.bands);
-    upload(s);
+    {   // verify_state (host, ~1 ms per million su) runs while the state is on its way to the device; a
+        // rejected state throws before any tick runs, exactly as if it had been checked first
+        std::exception_ptr rejected, upload_failed;
+        std::thread checker([&] {
+            try {
+                verify_state(s);
+            } catch (...) {
+                rejected = std::current_exception();
+            }
+        });
+        try {
+            upload(s);
+        } catch (...) {
+            upload_failed = std::current_exception();
+        }
+        checker.join();
+        if (rejected) std::rethrow_exception(rejected);
+        if (upload_failed) std::rethrow_exception(upload_failed);
+    }
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
     const int status = sfc_run(dev_, ticks, raw.data(), 0);
     download(s);
@@ -647,6 +673,40 @@ std::array<StrengthImage, kDynKinds> Engine::rebuild_images(const SimState& s) c
 void Engine::verify_state(const SimState& s) const {
     const auto reject = [&s](const std::string& what) { throw IntegrityError(what, s.tick, 0); };
     if (!(s.occupancy.geometry() == geom_)) reject("occupancy geometry mismatch");
+    {   // Fast acceptance of a consistent state (every run() starts here): each pedestrian is well-formed and
+        // every su of its body holds its id, and the grid holds no other occupant.  Anything else falls
+        // through to the reference's check below, which finds the FIRST violation in its order and words it.
+        const auto& occ = s.occupancy.raw();
+        const std::size_t w = static_cast<std::size_t>(geom_.width);
+        bool fine = true;
+        std::size_t body_cells = 0;
+        for (std::size_t i = 0; i < s.pedestrians.size() && fine; ++i) {
+            const Pedestrian& p = s.pedestrians[i];
+            fine = p.id == static_cast<std::int32_t>(i) && p.center.x >= 0 && p.center.x < geom_.width && p.center.y >= 0 &&
+                   p.center.y < geom_.height && p.walk_period >= 1 && p.walk_phase >= 0 && p.walk_phase < p.walk_period &&
+                   p.goal_sect >= 0 && p.goal_sect < kSects;
+            for (int k = 0; k < kDynKinds && fine; ++k) {
+                const FieldSpec& have = p.dyn_fields[static_cast<std::size_t>(k)];
+                const FieldSpec& want = field_templates_[static_cast<std::size_t>(k)];
+                fine = have.kind == want.kind && have.geometry == want.geometry && have.gain == want.gain && have.decay == want.decay;
+            }
+            if (!fine) break;
+            if (p.footprint.width == 1 && p.footprint.height == 1) {
+                fine = occ[static_cast<std::size_t>(p.center.y) * w + static_cast<std::size_t>(p.center.x)] == p.id;
+                body_cells += 1;
+            } else {
+                const FootprintCells body = footprint_cells(geom_, p.center, p.footprint);
+                fine = !body.clipped;
+                for (const SuIndex su : body.cells) fine = fine && s.occupancy.at(su) == p.id;
+                body_cells += body.cells.size();
+            }
+        }
+        if (fine) {
+            std::size_t occupied = 0;
+            for (const std::int32_t id : occ) occupied += id != kNoPedestrian;
+            if (occupied == body_cells) return; // (a body wrapping onto itself repeats su: counts differ, slow path words it)
+        }
+    }
     OccupancyGrid expected(geom_);
     for (std::size_t i = 0; i < s.pedestrians.size(); ++i) {
         const Pedestrian& p = s.pedestrians[i];

@@ -195,6 +195,26 @@ std::vector<Offset> support(const FieldSpec& f) {
     return cells;
 }
 
+namespace detail {
+
+void HostPin::ensure(const void* p, std::size_t bytes) noexcept {
+    if (p == ptr_ && bytes == bytes_) return;
+    release();
+    if (p == nullptr || bytes < (std::size_t{1} << 20)) return;
+    if (sfc_host_pin(p, bytes) == 0) {
+        ptr_ = p;
+        bytes_ = bytes;
+    }
+}
+
+void HostPin::release() noexcept {
+    if (ptr_ != nullptr) sfc_host_unpin(ptr_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+}
+
+} // namespace detail
+
 StrengthImage::StrengthImage(const GridGeometry& g)
     : shape_(g), v_(static_cast<std::size_t>(g.cells()) * kSects, 0.0f) {}
 
