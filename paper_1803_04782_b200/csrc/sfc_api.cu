@@ -98,6 +98,7 @@ struct sfc_engine {
     int pairs_red = 0;        // its RED variant is exact for the uploaded state (sfc_upload)
     int pairs_red_tables = 0; // ... as far as the field magnitudes go (all >= 2^-40: sums are multiples of 2^-115)
     int pairs_red_pref = -1;  // SFC_K5_RED: 0 never, 1 always (tests), -1 when provably exact
+    int negative_zero = 0;    // the uploaded images held a -0.0f (Ctl::negative_zero): runs end with the normalising pass
     FieldTables field{};      // tables of the large-field kernel (blob == nullptr: not available for these tables)
     int k5_field = 0;         // the large-field kernel is the k-5 kernel (chosen in sfc_upload)
     int field_ctas[2] = {148, 148}; // its persistent grids ([1]: the lazy shape)
@@ -927,6 +928,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
     }
     int tiny = 0;
     SFC_CUDA(cudaMemcpyAsync(&tiny, &e->ctl->tiny_image, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    SFC_CUDA(cudaMemcpyAsync(&e->negative_zero, &e->ctl->negative_zero, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
     SFC_CUDA(cudaStreamSynchronize(e->stream)); // gate/attr staging vectors die here
     {   // float reductions at the L2 flush subnormals: exact only while no image value can be one
         const int red = e->pairs_red_pref >= 0 ? e->pairs_red_pref : (e->pairs_red_tables && !tiny);
@@ -1051,6 +1053,10 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
             if (rc != SFC_OK) return rc;
         }
     }
+    if (e->negative_zero && !e->slab.active) { // (the reference's k-5 turns every -0.0f into +0.0f once anybody moved)
+        SFC_CUDA(launch_normalize_negative_zero(e->stream, e->dyn, e->cells, e->ctl, e->moved_counts, 0, ticks));
+        e->counters.kernel_launches += 2;
+    }
     SFC_CUDA(cudaEventRecord(e->ev_stop, e->stream));
     std::vector<unsigned long long> moved;
     if (metrics) {
@@ -1118,6 +1124,10 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
         case 5:
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 0)));
             e->counters.kernel_launches += e->k5_launches;
+            if (e->negative_zero && !e->slab.active) {
+                SFC_CUDA(launch_normalize_negative_zero(e->stream, e->dyn, e->cells, e->ctl, e->moved_counts, 0, 1));
+                e->counters.kernel_launches += 2;
+            }
             break;
         case 6: {
             SFC_CUDA(launch_tick_advance(e->stream, e->ctl));

@@ -140,6 +140,9 @@ struct Ctl {
     unsigned int epoch;      // k-5: this tick's tile stamp (set by k-3, read by k-4 and k-5; never 0)
     int tiny_image;          // upload: an uploaded dynamic-image value is non-zero below 2^-92 — sums could be
                              // subnormal, so k-5 may not use flush-to-zero float reductions (sfc_k5_pairs.cu)
+    int negative_zero;       // upload: a dynamic-image value is -0.0f.  The reference's k-5 adds (float)total to EVERY
+                             // address once anybody moved (engine.cpp:468,524), which turns -0.0f into +0.0f; k-5 here skips
+                             // untouched addresses, so the first moving tick is followed by one normalising pass
 };
 
 // Optional reference-shaped temporaries for the Inspector path (engine.hpp:172-177).
@@ -328,6 +331,9 @@ cudaError_t launch_interleave(cudaStream_t s, const float* plane, float* dyn, in
 cudaError_t launch_deinterleave(cudaStream_t s, const float* dyn, float* plane, int kind, long long cells_begin,
                                 long long cells);
 cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v);
+// -0.0f -> +0.0f over the dynamic images if Ctl::negative_zero is set and a tick of [first, first + ticks) moved anybody
+cudaError_t launch_normalize_negative_zero(cudaStream_t s, float* dyn, long long cells, Ctl* ctl, const unsigned long long* moved_counts,
+                                           long long first, long long ticks);
 cudaError_t launch_occupancy_from_peds(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ);
 cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl);
 cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,

@@ -211,30 +211,55 @@ k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, in
         int qd[8];
 #pragma unroll
         for (int slot = 0; slot < 8; ++slot) qd[slot] = (q[slot] >= 0 && q[slot] != (int)i) ? (int)p.dir[q[slot]] : -2;
-        bool won1 = true;
+        // the reference's scan of the su's slots in slot order (first registrant seeds the best, then strictly
+        // greater score, then the id tie-break): kept as a scan so that NaN scores order exactly as there
+        double theirs[8];
+#pragma unroll
+        for (int slot = 0; slot < 8; ++slot) theirs[slot] = qd[slot] == slot ? p.score[q[slot]] : 0.0;
+        int best_id = kNoPed;
+        double best = 0.0;
 #pragma unroll
         for (int slot = 0; slot < 8; ++slot) {
-            if (qd[slot] != slot) continue; // not a registrant of my su
-            const double theirs = p.score[q[slot]];
-            if (theirs > my) won1 = false;
-            if (theirs == my && (fault ? q[slot] > (int)i : q[slot] < (int)i)) won1 = false;
+            const bool me = slot == d;
+            if (!me && qd[slot] != slot) continue; // not a registrant of my su
+            const int id = me ? (int)i : q[slot];
+            const double score = me ? my : theirs[slot];
+            bool better = best_id == kNoPed || score > best;
+            if (!better && score == best) better = fault ? id > best_id : id < best_id;
+            if (better) {
+                best_id = id;
+                best = score;
+            }
         }
-        p.won[i] = won1 ? 1 : 0;
+        p.won[i] = best_id == (int)i ? 1 : 0;
         return;
     }
     const bool won = for_new_cells(c.x, c.y, attr_half_w(attr), attr_half_h(attr), d, [&](int x, int y) {
+        int best_id = kNoPed;
+        double best = 0.0;
 #pragma unroll
-        for (int slot = 0; slot < 8; ++slot) {
-            const long long idx = cell_index(g, x - step_dx(slot), y - step_dy(slot));
-            if (idx < 0) continue;
-            const int q = occ[idx];
-            if (q < 0 || q == (int)i) continue;
-            if (p.dir[q] != slot) continue;
-            const double theirs = p.score[q];
-            if (theirs > my) return false;
-            if (theirs == my && (fault ? q > (int)i : q < (int)i)) return false;
+        for (int slot = 0; slot < 8; ++slot) { // (slot order, as the reference scans them)
+            int id;
+            double score;
+            if (slot == d) {
+                id = (int)i;
+                score = my;
+            } else {
+                const long long idx = cell_index(g, x - step_dx(slot), y - step_dy(slot));
+                if (idx < 0) continue;
+                id = occ[idx];
+                if (id < 0 || id == (int)i) continue;
+                if (p.dir[id] != slot) continue;
+                score = p.score[id];
+            }
+            bool better = best_id == kNoPed || score > best;
+            if (!better && score == best) better = fault ? id > best_id : id < best_id;
+            if (better) {
+                best_id = id;
+                best = score;
+            }
         }
-        return true;
+        return best_id == (int)i;
     });
     p.won[i] = won ? 1 : 0;
 }
@@ -449,6 +474,38 @@ __global__ void interleave_kernel(const float* __restrict__ plane, float* __rest
     const float lo = fminf(fminf(v.x != 0.f ? fabsf(v.x) : 1.f, v.y != 0.f ? fabsf(v.y) : 1.f),
                            fminf(v.z != 0.f ? fabsf(v.z) : 1.f, v.w != 0.f ? fabsf(v.w) : 1.f));
     if (lo < kTinyImage && ctl->tiny_image == 0) ctl->tiny_image = 1;
+    const bool nz = __float_as_uint(v.x) == 0x80000000u || __float_as_uint(v.y) == 0x80000000u || __float_as_uint(v.z) == 0x80000000u ||
+                    __float_as_uint(v.w) == 0x80000000u;
+    if (nz && ctl->negative_zero == 0) ctl->negative_zero = 1;
+}
+
+// See Ctl::negative_zero.  x + (+0.0f) = x for every x but -0.0f, so the reference's unconditional add is this pass.
+__global__ void normalize_negative_zero_kernel(float* __restrict__ dyn, long long n4, const Ctl* ctl,
+                                               const unsigned long long* __restrict__ moved_counts, long long first, long long ticks) {
+    if (ctl->negative_zero == 0 || ctl->error_code != 0) return;
+    bool moved = false;
+    for (long long t = 0; t < ticks && !moved; ++t) moved = moved_counts[first + t] != 0ull;
+    if (!moved) return;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        float4 v = reinterpret_cast<float4*>(dyn)[i];
+        const bool nz = __float_as_uint(v.x) == 0x80000000u || __float_as_uint(v.y) == 0x80000000u || __float_as_uint(v.z) == 0x80000000u ||
+                        __float_as_uint(v.w) == 0x80000000u;
+        if (!nz) continue;
+        v.x = __fadd_rn(v.x, 0.0f);
+        v.y = __fadd_rn(v.y, 0.0f);
+        v.z = __fadd_rn(v.z, 0.0f);
+        v.w = __fadd_rn(v.w, 0.0f);
+        reinterpret_cast<float4*>(dyn)[i] = v;
+    }
+}
+
+__global__ void negative_zero_done_kernel(Ctl* ctl, const unsigned long long* __restrict__ moved_counts, long long first, long long ticks) {
+    if (ctl->negative_zero == 0 || ctl->error_code != 0) return;
+    for (long long t = 0; t < ticks; ++t)
+        if (moved_counts[first + t] != 0ull) {
+            ctl->negative_zero = 0;
+            return;
+        }
 }
 
 __global__ void deinterleave_kernel(const float* __restrict__ dyn, float* __restrict__ plane, int kind, long long cells) {
@@ -543,6 +600,15 @@ cudaError_t launch_occupancy_from_peds(cudaStream_t s, const GridDev& g, const P
 
 cudaError_t launch_fill_i8(cudaStream_t s, int8_t* p, long long n, int v) {
     fill_i8_kernel<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_negative_zero(cudaStream_t s, float* dyn, long long cells, Ctl* ctl, const unsigned long long* moved_counts,
+                                           long long first, long long ticks) {
+    const long long n4 = cells * (kKinds * kSects / 4);
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148 * 8);
+    normalize_negative_zero_kernel<<<std::max(blocks, 1), 256, 0, s>>>(dyn, n4, ctl, moved_counts, first, ticks);
+    negative_zero_done_kernel<<<1, 1, 0, s>>>(ctl, moved_counts, first, ticks);
     return cudaGetLastError();
 }
 

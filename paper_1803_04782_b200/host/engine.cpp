@@ -272,6 +272,22 @@ void Engine::require_device() const {
     const_cast<Engine*>(this)->dev_ = bridge::create_engine(geom_, cfg_, tables);
 }
 
+namespace {
+
+// The reference's k-5 adds (float)total to every image address once anybody moved (engine.cpp:468,524), which
+// turns a -0.0f entry into +0.0f; the device kernels skip untouched addresses.  Paths that run from host
+// state finish with this pass instead (the resident path does it on the device, Ctl::negative_zero).
+void normalize_negative_zero(SimState& s, const std::vector<sfc_tick_metrics>& ticks) {
+    bool moved = false;
+    for (const sfc_tick_metrics& t : ticks) moved = moved || t.moved > 0;
+    if (!moved) return;
+    for (StrengthImage& img : s.dyn_images)
+        for (float& v : img.raw_mut())
+            if (v == 0.0f) v = 0.0f; // (-0.0f == 0.0f: rewritten as +0.0f)
+}
+
+} // namespace
+
 // run() for a state that does not fit the device: the caller's host SimState is the backing store and
 // the SU grid streams through the device in row bands, one phase at a time (sfc_band_run).
 std::vector<TickMetrics> Engine::run_bands(SimState& s, long ticks, int bands) {
@@ -321,6 +337,7 @@ std::vector<TickMetrics> Engine::run_bands(SimState& s, long ticks, int bands) {
     sfc_state_view v = make_view(s, cols);
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
     const int status = sfc_band_run(band_engine_, &v, ticks, raw.data());
+    normalize_negative_zero(s, raw);
     for (std::size_t i = 0; i < s.pedestrians.size(); ++i) s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
     s.tick = static_cast<long>(v.tick);
     if (status != SFC_OK) {
@@ -393,6 +410,7 @@ std::vector<TickMetrics> Engine::run_slabs(SimState& s, long ticks) {
         const int status = sfc_download(e, &v);
         if (status != SFC_OK) fail_with(e, status);
     }
+    if (run_status == SFC_OK) normalize_negative_zero(s, raw);
     for (std::size_t i = 0; i < s.pedestrians.size(); ++i) s.pedestrians[i].center = SuIndex{cols.center_xy[2 * i], cols.center_xy[2 * i + 1]};
     s.tick = static_cast<long>(v.tick);
     if (run_status != SFC_OK) fail_with(slab_engines_.front(), run_status);

@@ -208,6 +208,60 @@ def test_subnormal_image_values_stay_exact(product_lib):
         assert_state_equal(gpu, cpu, f"subnormal tick {4 * (step + 1)}")
 
 
+@pytest.mark.parametrize("path", ["pairs", "scatter", "window", "field", "slabs", "bands"])
+def test_negative_zero_image_entries_are_normalised_like_the_reference(product_lib, monkeypatch, path):
+    """The reference's k-5 adds (float)total to EVERY (su, kind, sect) address once anybody moved
+    (engine.cpp:468,524): a -0.0f entry — only reachable through the public mutable SimState — becomes
+    +0.0f at the first moving tick, and stays -0.0f while nobody moves.  The device kernels skip
+    untouched addresses, so a normalising pass follows the first moving tick: bit-identical images."""
+    if path == "slabs":
+        monkeypatch.setenv("SFC_SLABS", "2")
+    elif path == "bands":
+        monkeypatch.setenv("SFC_BANDS", "2")
+    else:
+        monkeypatch.setenv("SFC_K5_PATH", path)
+    text = sc.variant(sc.DESK64, rebuild_interval=0, density=0.05, walk_period="3..3")
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    rng = np.random.default_rng(11)
+    for k in range(3):
+        img = cpu.image(k).copy()
+        zero = (img == 0.0) & (rng.random(img.shape) < 0.4)
+        img[zero] = -0.0
+        assert np.signbit(img[zero]).all()
+        cpu.image(k)[:] = img
+        gpu.set_image(k, img)
+    for step in range(4):
+        np.testing.assert_array_equal(gpu.run(2), cpu.run(2))
+        assert_state_equal(gpu, cpu, f"negative zero, {path}, tick {2 * (step + 1)}")
+
+
+def test_nan_scores_order_like_the_reference(product_lib):
+    """NaN image values (only reachable through the public mutable SimState) give NaN scores, which the
+    reference's vote orders by slot position: the first registrant seeds the best, a later NaN never
+    beats it, a seeded NaN is never beaten (engine.cpp:365-386).  The vote here is the same scan, so
+    decisions, winners and positions agree; the images agree wherever they are numbers (a NaN's payload
+    is not portable between x86 and the GPU's adders)."""
+    text = sc.variant(sc.DESK64, rebuild_interval=0, density=0.6)
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    rng = np.random.default_rng(12)
+    for k in range(3):
+        img = cpu.image(k).copy()
+        img[rng.random(img.shape) < 0.02] = np.nan
+        cpu.image(k)[:] = img
+        gpu.set_image(k, img)
+    for step in range(5):
+        np.testing.assert_array_equal(gpu.run(3), cpu.run(3), err_msg="moved")
+        np.testing.assert_array_equal(gpu.centers(), cpu.centers(), err_msg=f"tick {gpu.tick} centres")
+        np.testing.assert_array_equal(gpu.occupancy(), cpu.occupancy(), err_msg=f"tick {gpu.tick} occupancy")
+        for k in range(3):
+            a, b = gpu.image(k), cpu.image(k)
+            np.testing.assert_array_equal(np.isnan(a), np.isnan(b))
+            np.testing.assert_array_equal(bits(np.where(np.isnan(a), 0.0, a).astype(np.float32)),
+                                          bits(np.where(np.isnan(b), 0.0, b).astype(np.float32)))
+
+
 def test_default_path_field13(product_lib):
     """13 x 13 fields in a crowd, no knobs: scatter kernel, crowded tiles handed to the list walk."""
     text = sc.EXTRA["field13-crowd"]
