@@ -400,8 +400,9 @@ int check_device_error(sfc_engine* e) {
         std::snprintf(buf, sizeof buf, "device error %d in phase 4: event list of the slab overflowed (%g entries)", h.error_code,
                       h.error_value);
     } else {
-        std::snprintf(buf, sizeof buf, "device error %d in phase %d (rebuild list capacity exceeded: %g centres)",
-                      h.error_code, h.error_phase, h.error_value);
+        std::snprintf(buf, sizeof buf, "device error %d in phase %d%s (%g)", h.error_code, h.error_phase,
+                      h.error_phase == 5 ? ": a rebuild tile sees more centres of one id range than its sorted list holds" : "",
+                      h.error_value);
     }
     e->err = buf;
     return h.error_code;

@@ -11,6 +11,9 @@
 // them by (id, -y, -x) in shared memory (bitonic network on 64-bit keys), and every su walks
 // the sorted list adding the table magnitudes in float — atomics-free and bit-exact.
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "sfc_internal.cuh"
 
 namespace sfc {
@@ -56,78 +59,92 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     const bool active = lx < nx && ly < ny;
     const int tcx = lx + HW, tcy = ly + HH;
 
-    if (tid == 0) s_count = 0;
-    for (int i = tid; i < a.cap; i += kRbThreads) keys[i] = ~0ull;
 #pragma unroll
     for (int q = 0; q < kKinds * kSects; ++q) acc[q * kRbThreads + tid] = 0.0f;
-    __syncthreads();
 
-    // collect the pedestrian centres of the region (any order; sorted below)
+    // The centres of the region are taken in ROUNDS of ascending id ranges: one round over every id when
+    // they fit the sorted list (the usual case), else as many equal id ranges as bring a range's expected
+    // share under half the capacity — per-address order is ascending id either way, so the float sums are
+    // the reference's.  (Ids are handed out in placement order, i.e. uniformly over the grid.)
     const int ncell = RW * RH;
-    for (int i = tid; i < ncell; i += kRbThreads) {
-        const int ryi = i / RW, rxi = i - ryi * RW;
-        const long long idx = cell_index(g, xs + rxi, ys + ryi);
-        if (idx < 0) continue;
-        const int id = a.occ[idx];
-        if (id < 0) continue;
-        const int2 c = a.p.center[id];
-        int wx = xs + rxi, wy = ys + ryi;
-        if (!g.closed) {
-            wx = emod(wx, g.W);
-            wy = emod(wy, g.H);
+    int rounds = 1;
+    for (int round = 0; round < rounds; ++round) {
+        const long long id_lo = rounds == 1 ? 0 : a.p.n * round / rounds, id_hi = rounds == 1 ? a.p.n : a.p.n * (round + 1) / rounds;
+        __syncthreads(); // (the previous round's walk is done with the keys)
+        if (tid == 0) s_count = 0;
+        for (int i = tid; i < a.cap; i += kRbThreads) keys[i] = ~0ull;
+        __syncthreads();
+        // collect the pedestrian centres of the region (any order; sorted below)
+        for (int i = tid; i < ncell; i += kRbThreads) {
+            const int ryi = i / RW, rxi = i - ryi * RW;
+            const long long idx = cell_index(g, xs + rxi, ys + ryi);
+            if (idx < 0) continue;
+            const int id = a.occ[idx];
+            if (id < id_lo || id >= id_hi) continue; // (empty su hold -1)
+            const int2 c = a.p.center[id];
+            int wx = xs + rxi, wy = ys + ryi;
+            if (!g.closed) {
+                wx = emod(wx, g.W);
+                wy = emod(wy, g.H);
+            }
+            if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
+            const int pos = atomicAdd(&s_count, 1);
+            if (pos < a.cap) {
+                const uint32_t attr = a.p.attr[id];
+                keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
+                            ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+            }
         }
-        if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
-        const int pos = atomicAdd(&s_count, 1);
-        if (pos < a.cap) {
-            const uint32_t attr = a.p.attr[id];
-            keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
-                        ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+        __syncthreads();
+        const int n = s_count;
+        if (n > a.cap) {
+            if (rounds == 1) { // too many centres for one sorted list: split the id range and start over
+                rounds = min(4096, 2 * ((n + a.cap - 1) / a.cap));
+                round = -1;
+                continue;
+            }
+            if (tid == 0) raise_error(a.ctl, SFC_E_STATE, 5, x0, y0, (double)n);
+            return;
         }
-    }
-    __syncthreads();
-    const int n = s_count;
-    if (n > a.cap) {
-        if (tid == 0) raise_error(a.ctl, SFC_E_STATE, 5, x0, y0, (double)n);
-        return;
-    }
-    // bitonic sort of the first pow2 >= n keys (padding keys are all-ones)
-    int m = 1;
-    while (m < n) m <<= 1;
-    for (int k = 2; k <= m; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < m; i += kRbThreads) {
-                const int partner = i ^ j;
-                if (partner > i) {
-                    const unsigned long long ka = keys[i], kb = keys[partner];
-                    const bool up = (i & k) == 0;
-                    if ((ka > kb) == up) {
-                        keys[i] = kb;
-                        keys[partner] = ka;
+        // bitonic sort of the first pow2 >= n keys (padding keys are all-ones)
+        int m = 1;
+        while (m < n) m <<= 1;
+        for (int k = 2; k <= m; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < m; i += kRbThreads) {
+                    const int partner = i ^ j;
+                    if (partner > i) {
+                        const unsigned long long ka = keys[i], kb = keys[partner];
+                        const bool up = (i & k) == 0;
+                        if ((ka > kb) == up) {
+                            keys[i] = kb;
+                            keys[partner] = ka;
+                        }
                     }
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
-    }
 
-    if (active && n > 0) {
-        for (int e = 0; e < n; ++e) {
-            const unsigned long long key = keys[e];
-            const int ry = 8191 - (int)((key >> 19) & 0x1FFF), rx = 8191 - (int)((key >> 6) & 0x1FFF);
-            const int dx = rx - tcx, dy = ry - tcy; // centre offset = centre - target
-            if ((dx | dy) == 0) continue;
-            const uint32_t orients = (uint32_t)(key & 0x3F);
+        if (active && n > 0) {
+            for (int e = 0; e < n; ++e) {
+                const unsigned long long key = keys[e];
+                const int ry = 8191 - (int)((key >> 19) & 0x1FFF), rx = 8191 - (int)((key >> 6) & 0x1FFF);
+                const int dx = rx - tcx, dy = ry - tcy; // centre offset = centre - target
+                if ((dx | dy) == 0) continue;
+                const uint32_t orients = (uint32_t)(key & 0x3F);
 #pragma unroll
-            for (int kind = 0; kind < kKinds; ++kind) {
-                const KindTableDev kt = a.t.k[kind];
-                if (dx < -kt.hw || dx > kt.hw || dy < -kt.hh || dy > kt.hh) continue;
-                const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
-                const uint32_t info = __ldg(kt.info + ti);
-                const uint32_t mask = (info >> 3) & 0xFFu;
-                const int orient = kind == 0 ? (orients & 7) : (kind == 1 ? ((orients >> 3) & 7) : 0);
-                if (!((mask >> orient) & 1u)) continue;
-                float* slot = acc + (kind * kSects + (info & 7)) * kRbThreads + tid;
-                *slot = __fadd_rn(*slot, __double2float_rn(__ldg(kt.mag + ti))); // += (float)s.norm()
+                for (int kind = 0; kind < kKinds; ++kind) {
+                    const KindTableDev kt = a.t.k[kind];
+                    if (dx < -kt.hw || dx > kt.hw || dy < -kt.hh || dy > kt.hh) continue;
+                    const int ti = (dy + kt.hh) * kt.fw + dx + kt.hw;
+                    const uint32_t info = __ldg(kt.info + ti);
+                    const uint32_t mask = (info >> 3) & 0xFFu;
+                    const int orient = kind == 0 ? (orients & 7) : (kind == 1 ? ((orients >> 3) & 7) : 0);
+                    if (!((mask >> orient) & 1u)) continue;
+                    float* slot = acc + (kind * kSects + (info & 7)) * kRbThreads + tid;
+                    *slot = __fadd_rn(*slot, __double2float_rn(__ldg(kt.mag + ti))); // += (float)s.norm()
+                }
             }
         }
     }
@@ -250,6 +267,8 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     a.mode = mode;
     a.tiles_x = (g.W + kTileW - 1) / kTileW;
     a.cap = rebuild_cap(t);
+    if (const char* knob = std::getenv("SFC_REBUILD_CAP")) // (tests: a short sorted list forces the id-range rounds)
+        a.cap = std::min(a.cap, next_pow2(std::max(1, std::atoi(knob))));
     const size_t smem = rebuild_smem(t);
     const long long blocks = (long long)a.tiles_x * ((g.rows + kRbTileH - 1) / kRbTileH);
     rebuild_kernel<<<(unsigned)blocks, kRbThreads, smem, s>>>(a);

@@ -262,6 +262,21 @@ def test_nan_scores_order_like_the_reference(product_lib):
                                           bits(np.where(np.isnan(b), 0.0, b).astype(np.float32)))
 
 
+@pytest.mark.parametrize("name", ["desk64", "field21", "d0.9-eight-ped1", "closed-four"])
+def test_rebuild_with_more_centres_than_its_sorted_list_holds(product_lib, monkeypatch, name):
+    """The rebuild sorts the centres of a tile's region by id in shared memory; when a region holds more
+    than the list does (large fields in dense crowds), it takes them in rounds of ascending id ranges —
+    the per-address order is ascending id either way.  Forced with a 32-entry list; bit-identical."""
+    monkeypatch.setenv("SFC_REBUILD_CAP", "32")
+    text = sc.variant(sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name], rebuild_interval=3)
+    gpu = shim.Sim.from_scenario(product_lib, text)  # (seeding rasterises through the same kernel)
+    cpu = oracle.OracleSim.from_scenario(text)
+    assert_state_equal(gpu, cpu, f"{name} seed")
+    for step in range(3):
+        np.testing.assert_array_equal(gpu.run(4), cpu.run(4))
+        assert_state_equal(gpu, cpu, f"{name} tick {4 * (step + 1)}")
+
+
 def test_default_path_field13(product_lib):
     """13 x 13 fields in a crowd, no knobs: scatter kernel, crowded tiles handed to the list walk."""
     text = sc.EXTRA["field13-crowd"]
