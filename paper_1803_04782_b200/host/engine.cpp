@@ -262,7 +262,22 @@ Engine::Engine(const GridGeometry& g, const EngineConfig& cfg, const std::array<
 Engine::~Engine() {
     release_slabs();
     if (band_engine_) sfc_destroy(band_engine_);
+    if (probe_engine_) sfc_destroy(probe_engine_);
     if (dev_) sfc_destroy(dev_);
+}
+
+// decide() and rebuild_images() are const probes in the reference; here they upload the state they are
+// given.  While the caller steps a resident state (upload / seed_resident ... step_resident) that upload
+// must not land on it: the probes then use a scratch engine of their own.
+sfc_engine* Engine::probe_device() const {
+    require_device();
+    if (!resident_live_) return dev_;
+    if (!probe_engine_) {
+        std::array<bridge::KindTable, kDynKinds> tables;
+        for (int k = 0; k < kDynKinds; ++k) tables[static_cast<std::size_t>(k)] = bridge::build_kind_table(field_templates_[static_cast<std::size_t>(k)]);
+        probe_engine_ = bridge::create_engine(geom_, cfg_, tables);
+    }
+    return probe_engine_;
 }
 
 void Engine::require_device() const {
@@ -307,6 +322,7 @@ std::vector<TickMetrics> Engine::run_bands(SimState& s, long ticks, int bands) {
             std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
             const int status = sfc_run(dev_, ticks, raw.data(), 0);
             download(s);
+            resident_live_ = false;
             if (status != SFC_OK) throw_status(status);
             std::vector<TickMetrics> metrics;
             for (const auto& r : raw) metrics.push_back(to_metrics(r));
@@ -440,6 +456,7 @@ void Engine::upload(const SimState& s) {
     const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);
     const int status = sfc_upload(dev_, &v);
     if (status != SFC_OK) throw_status(status);
+    resident_live_ = true; // (run() / tick() clear it again: after their download the host state is authoritative)
     if (decisions_.size() != s.pedestrians.size()) decisions_.assign(s.pedestrians.size(), kStill);
 }
 
@@ -480,6 +497,7 @@ void Engine::seed_resident(const std::vector<Pedestrian>& pedestrians, long tick
     const sfc_state_view v = population_view(pedestrians, tick, cols);
     const int status = sfc_upload(dev_, &v);
     if (status != SFC_OK) throw_status(status);
+    resident_live_ = true;
     decisions_.assign(pedestrians.size(), kStill);
 }
 
@@ -570,6 +588,7 @@ void Engine::pull_temporaries(int phase, SimState& s) {
     if (phase >= 4) {
         const long tick_before = s.tick;
         download(s);
+        resident_live_ = false;
         s.tick = tick_before; // the counter advances only at the end of the tick
     }
 }
@@ -586,6 +605,7 @@ TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect
         sfc_tick_metrics raw{};
         status = sfc_run(dev_, 1, &raw, 1);
         download(s); // the state is meaningful even when the tick ended in an integrity error
+        resident_live_ = false;
         if (status != SFC_OK) throw_status(status);
         return to_metrics(raw);
     }
@@ -595,6 +615,7 @@ TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect
         const int status = sfc_phase(dev_, phase, phase >= 4 ? &moved : nullptr);
         if (status != SFC_OK) {
             download(s);
+            resident_live_ = false;
             throw_status(status);
         }
         if (phase >= 4) m.moved = moved;
@@ -603,6 +624,7 @@ TickMetrics Engine::tick(SimState& s, RunMode /*mode*/, const Inspector& inspect
     }
     const int status = sfc_phase(dev_, 6, nullptr);
     download(s);
+    resident_live_ = false;
     if (status != SFC_OK) throw_status(status);
     return m;
 }
@@ -644,6 +666,7 @@ std::vector<TickMetrics> Engine::run(SimState& s, long ticks, RunMode mode, cons
     std::vector<sfc_tick_metrics> raw(static_cast<std::size_t>(ticks));
     const int status = sfc_run(dev_, ticks, raw.data(), 0);
     download(s);
+    resident_live_ = false;
     if (status != SFC_OK) throw_status(status);
     metrics.reserve(raw.size());
     for (const auto& r : raw) metrics.push_back(to_metrics(r));
@@ -661,12 +684,13 @@ MoveDecision Engine::decide(const Pedestrian& p, const SimState& s) const {
     probe.pedestrians[slot] = p;
     bridge::PedColumns cols;
     const sfc_state_view v = make_view(probe, cols);
-    int status = sfc_upload(dev_, &v);
-    if (status != SFC_OK) throw_status(status);
+    sfc_engine* const dev = probe_device();
+    int status = sfc_upload(dev, &v);
+    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(dev), s.tick, 0);
     MoveDecision d;
     std::int32_t dir = kStill;
-    status = sfc_decide(dev_, p.id, &dir, &d.score);
-    if (status != SFC_OK) throw_status(status);
+    status = sfc_decide(dev, p.id, &dir, &d.score);
+    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(dev), s.tick, 2);
     d.direction = dir;
     if (dir != kStill) d.new_cells = newly_covered(geom_, p, dir);
     return d;
@@ -677,12 +701,13 @@ std::array<StrengthImage, kDynKinds> Engine::rebuild_images(const SimState& s) c
     require_shape(s, geom_);
     bridge::PedColumns cols;
     const sfc_state_view v = make_view(const_cast<SimState&>(s), cols);
-    int status = sfc_upload(dev_, &v);
-    if (status != SFC_OK) throw_status(status);
+    sfc_engine* const dev = probe_device();
+    int status = sfc_upload(dev, &v);
+    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(dev), s.tick, 0);
     std::array<StrengthImage, kDynKinds> fresh{StrengthImage(geom_), StrengthImage(geom_), StrengthImage(geom_)};
     float* out[kDynKinds] = {fresh[0].raw_mut().data(), fresh[1].raw_mut().data(), fresh[2].raw_mut().data()};
-    status = sfc_rasterize_dynamic(dev_, out);
-    if (status != SFC_OK) throw_status(status);
+    status = sfc_rasterize_dynamic(dev, out);
+    if (status != SFC_OK) bridge::throw_status(status, sfc_last_error(dev), s.tick, 0);
     return fresh;
 }
 

@@ -554,3 +554,4 @@ def test_validate_tool_exit_codes(tmp_path, capsys):
     dense.write_text("grid = 10x10\ndensity = 1.5\n")
     assert validate.main([str(dense)]) == 2
     assert validate.main([str(tmp_path / "absent.scn")]) == 1
+
