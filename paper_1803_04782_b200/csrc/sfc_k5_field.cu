@@ -71,6 +71,7 @@ struct FieldArgs {
     uint32_t group_of_sect[kKinds]; // sect group feeding sect s of kind k in bits [3s, 3s + 3)
     int tiles_x, n_tiles, tile_h;
     int rw_max, nwords;           // region columns of a full tile; 32-bit words per column bit map
+    int cs_ints;                  // ints of the column-start block (two arrays of rw_max + 2; at least one per region row)
     int cap;                      // entries per list chunk (each of the two lists)
     int advance_tick;
     int vec_ok;                   // 16-byte event-map loads are aligned (W % 8 == 0)
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
     FieldEvent* const evl = reinterpret_cast<FieldEvent*>(smag + a.mag_bytes / 8); // [left: cap | arrived: cap]
     uint32_t* const colbits = reinterpret_cast<uint32_t*>(evl + 2 * a.cap);        // [column][left words | arrived words]
     int* const colstart = reinterpret_cast<int*>(colbits + a.rw_max * 2 * a.nwords); // [left: rw_max + 2 | arrived: rw_max + 2]
-    uint32_t* const lut = reinterpret_cast<uint32_t*>(colstart + 2 * (a.rw_max + 2));
+    uint32_t* const lut = reinterpret_cast<uint32_t*>(colstart + a.cs_ints);
+    int* const rowlocal = colstart; // staging only (before the scan writes colstart): resident row of each region row, -1: no such row
     uint8_t* const tab8 = reinterpret_cast<uint8_t*>(lut + kSects);
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(a.blob);
@@ -129,6 +131,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
 
         // ---- stage: per-column bit maps of the region's events ---------------------------------
         for (int i = tid; i < RW * CW; i += NT) colbits[i] = 0u;
+        for (int ry = tid; ry < RH; ry += NT) {
+            const long long at = cell_index(g, 0, ys + ry);
+            rowlocal[ry] = at < 0 ? -1 : (int)(at / g.W);
+        }
         __syncthreads();
         {
             const int gx0 = (xs >> 3) * 8; // (arithmetic shift: floor for negative xs)
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
                         const int gx = gx0 + 8 * (i - ry * NG);
                         at_ry[q] = ry;
                         at_gx[q] = gx;
-                        const long long row = cell_index(g, 0, ys + ry); // -1: the row does not exist / is not resident
+                        const long long row = (long long)rowlocal[ry] * g.W; // negative: the row does not exist / is not resident
                         if (row < 0) {
                             at_ry[q] = -1;
                         } else if (a.vec_ok && gx >= 0 && gx + 8 <= g.W) {
@@ -215,7 +221,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
         }
         __syncthreads();
         const int n_left = colstart[RW], n_arrived = colstart[CS + RW];
-        if (n_left + n_arrived == 0) continue; // nobody moved within reach of this tile (uniform; colbits untouched until the next sync)
+        if (n_left + n_arrived == 0) { // nobody moved within reach of this tile (uniform)
+            __syncthreads();           // (the next tile's row table reuses the column-start block every thread just read)
+            continue;
+        }
 
         // ---- my block --------------------------------------------------------------------------
         const bool blk_ok = bx < nx && by < ny; // uniform per warp
@@ -230,6 +239,8 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
         const unsigned span_x = 2u * (unsigned)HW, span_y = 2u * (unsigned)HH;
         const FieldEvent* const my_list = evl + half * a.cap;
         const int* const my_cs = colstart + half * CS;
+        // my half (four sects) of my su's 96-byte record
+        float* const rec = a.dyn + (in_grid ? cell_index(g, x0 + cx, y0 + cy) : 0) * (kKinds * kSects) + 4 * half;
 
 #pragma unroll 1
         for (int kp = 0; kp < kKinds / NK; ++kp) {
@@ -246,6 +257,11 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
 #pragma unroll 8
                 for (int i = 0; i < NK * kSects * KH; ++i) part[i * 32] = 0.0;
             }
+            // thin crowds (latency-bound): the image sectors this pass will update are requested now and consumed after the walks
+            float4 old[NK];
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+                old[k] = LAZY && blk_live && in_grid ? *reinterpret_cast<const float4*>(rec + (NK == 1 ? kp : k) * kSects) : make_float4(0.f, 0.f, 0.f, 0.f);
 
             int c0 = 0;
             while (c0 < RW) {
@@ -352,15 +368,13 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
                 d_arrived[k] = half ? dirty[k] : other;
             }
             if (!in_grid || !any_su) continue;
-            const long long cell = cell_index(g, x0 + cx, y0 + cy);
-            float* const rec = a.dyn + cell * (kKinds * kSects) + 4 * half;
             const double* const pl = part - 16 * half; // the pair's "left" lane column (the "arrived" one is 16 further)
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 const int kind = NK == 1 ? kp : k;
                 if (LAZY && (d_left[k] | d_arrived[k]) == 0ull) continue;
                 float4* const r4 = reinterpret_cast<float4*>(rec + kind * kSects);
-                const float4 v = *r4;
+                const float4 v = LAZY ? old[k] : *r4;
                 float r[4] = {v.x, v.y, v.z, v.w};
                 const uint32_t gos = a.group_of_sect[kind] >> (12 * half);
 #pragma unroll
@@ -400,10 +414,12 @@ struct FieldShape {
     int nk, warps, cap, rw_max, nwords, tile_h;
 };
 
+int cs_ints(int rw_max, int rh_max) { return (std::max(2 * (rw_max + 2), rh_max) + 1) & ~1; }
+
 size_t fixed_bytes(const FieldTables& t, int tile_h) {
     const int rw_max = kTileW + 2 * t.hw, rh_max = tile_h + 2 * t.hh;
     const int nwords = (rh_max + 31) / 32;
-    return (size_t)t.mag_bytes + sizeof(uint32_t) * (size_t)rw_max * 2 * nwords + sizeof(int) * 2 * (size_t)(rw_max + 2) +
+    return (size_t)t.mag_bytes + sizeof(uint32_t) * (size_t)rw_max * 2 * nwords + sizeof(int) * (size_t)cs_ints(rw_max, rh_max) +
            sizeof(uint32_t) * kSects + (size_t)t.tab_bytes + 16;
 }
 
@@ -618,6 +634,7 @@ cudaError_t launch_k5_field(cudaStream_t s, const K5Launch& l) {
     a.n_tiles = a.tiles_x * ((l.g.rows + sh.tile_h - 1) / sh.tile_h);
     a.rw_max = sh.rw_max;
     a.nwords = sh.nwords;
+    a.cs_ints = cs_ints(sh.rw_max, sh.tile_h + 2 * t.hh);
     a.cap = l.list_cap > 0 ? std::clamp(l.list_cap, sh.tile_h + 2 * t.hh, sh.cap) : sh.cap;
     a.advance_tick = l.advance_tick;
     a.vec_ok = l.g.W % 8 == 0;
