@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
             // ---- fold: StepCache::total in slot order, image += (float)total -------------------
             // Slot 2 q lives with the su's "left" lane, slot 2 q + 1 with its "arrived" lane; each lane
             // of the pair folds four sects of every kind (one 16-byte sector half).
+            __syncwarp(); // the partner lane's partials are read below
             const int any_other = __shfl_xor_sync(0xFFFFFFFFu, (int)any, 16);
             const bool any_su = any || any_other != 0;
             unsigned long long d_left[NK], d_arrived[NK];
@@ -367,41 +368,43 @@ __global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
                 d_left[k] = half ? other : dirty[k];
                 d_arrived[k] = half ? dirty[k] : other;
             }
-            if (!in_grid || !any_su) continue;
-            const double* const pl = part - 16 * half; // the pair's "left" lane column (the "arrived" one is 16 further)
-#pragma unroll
-            for (int k = 0; k < NK; ++k) {
-                const int kind = NK == 1 ? kp : k;
-                if (LAZY && (d_left[k] | d_arrived[k]) == 0ull) continue;
-                float4* const r4 = reinterpret_cast<float4*>(rec + kind * kSects);
-                const float4 v = LAZY ? old[k] : *r4;
-                float r[4] = {v.x, v.y, v.z, v.w};
-                const uint32_t gos = a.group_of_sect[kind] >> (12 * half);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int grp = (int)((gos >> (3 * j)) & 7u);
-                    const double* const p = pl + k * KO + grp * (KH * 32);
-                    double total = 0.0;
-                    if (LAZY) {
-                        uint32_t ml = (uint32_t)(d_left[k] >> (grp * KH)) & ((1u << KH) - 1u);
-                        uint32_t ma = (uint32_t)(d_arrived[k] >> (grp * KH)) & ((1u << KH) - 1u);
-                        if ((ml | ma) == 0u) continue;
-#pragma unroll
-                        for (int q = 0; q < KH; ++q) { // slot order: 2 q, 2 q + 1
-                            if ((ml >> q) & 1u) total = __dadd_rn(total, p[q * 32]);
-                            if ((ma >> q) & 1u) total = __dadd_rn(total, p[q * 32 + 16]);
+            if (in_grid && any_su) {
+                const double* const pl = part - 16 * half; // the pair's "left" lane column (the "arrived" one is 16 further)
+    #pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    const int kind = NK == 1 ? kp : k;
+                    if (LAZY && (d_left[k] | d_arrived[k]) == 0ull) continue;
+                    float4* const r4 = reinterpret_cast<float4*>(rec + kind * kSects);
+                    const float4 v = LAZY ? old[k] : *r4;
+                    float r[4] = {v.x, v.y, v.z, v.w};
+                    const uint32_t gos = a.group_of_sect[kind] >> (12 * half);
+    #pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int grp = (int)((gos >> (3 * j)) & 7u);
+                        const double* const p = pl + k * KO + grp * (KH * 32);
+                        double total = 0.0;
+                        if (LAZY) {
+                            uint32_t ml = (uint32_t)(d_left[k] >> (grp * KH)) & ((1u << KH) - 1u);
+                            uint32_t ma = (uint32_t)(d_arrived[k] >> (grp * KH)) & ((1u << KH) - 1u);
+                            if ((ml | ma) == 0u) continue;
+    #pragma unroll
+                            for (int q = 0; q < KH; ++q) { // slot order: 2 q, 2 q + 1
+                                if ((ml >> q) & 1u) total = __dadd_rn(total, p[q * 32]);
+                                if ((ma >> q) & 1u) total = __dadd_rn(total, p[q * 32 + 16]);
+                            }
+                        } else {
+    #pragma unroll
+                            for (int q = 0; q < KH; ++q) {
+                                total = __dadd_rn(total, p[q * 32]);
+                                total = __dadd_rn(total, p[q * 32 + 16]);
+                            }
                         }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < KH; ++q) {
-                            total = __dadd_rn(total, p[q * 32]);
-                            total = __dadd_rn(total, p[q * 32 + 16]);
-                        }
+                        r[j] = __fadd_rn(r[j], __double2float_rn(total)); // engine.cpp:468
                     }
-                    r[j] = __fadd_rn(r[j], __double2float_rn(total)); // engine.cpp:468
+                    *r4 = make_float4(r[0], r[1], r[2], r[3]);
                 }
-                *r4 = make_float4(r[0], r[1], r[2], r[3]);
             }
+            __syncwarp(); // (the next pass rewrites partials the partner lane may still be folding)
         }
         __syncthreads(); // every walk is done before the next tile restages colbits / the lists
     }
