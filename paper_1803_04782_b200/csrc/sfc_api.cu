@@ -73,6 +73,7 @@ struct sfc_engine {
     int band_count = 0;    // > 1: band-swapped engine (sfc_band_run): g.row0 / g.rows move over the grid
     int band_rows = 0;     // rows of a full band (the last band may be shorter)
     std::vector<uint8_t> band_ev; // host backing of the event map (2 B per su of the whole grid)
+    unsigned* rebuild_changed = nullptr; // one bit per rebuild tile: the check pass marks the tiles the commit pass must write
     int* dense_list = nullptr; // k-5 tile ids handed from the scatter to the gather kernel
     int persistent_ctas = 148 * 3;
     int k5_launches = 1;       // kernels per k-5 phase
@@ -464,9 +465,12 @@ int enqueue_tick_kernels(sfc_engine* e) {
 }
 
 int enqueue_rebuild(sfc_engine* e) { // maybe_rebuild body, engine.cpp:540-549
-    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 1, 0.0));
+    // (the commit pass only rewrites tiles where the check pass saw a fresh value differ from the image: in a sparse
+    // crowd most tiles are all zero before and after)
+    unsigned* const changed = e->slab.band ? nullptr : e->rebuild_changed;
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 1, 0.0, changed));
     SFC_CUDA(launch_drift_verdict(e->stream, e->ctl, e->cfg.rebuild_tolerance));
-    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 2, 0.0));
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 2, 0.0, changed));
     e->counters.kernel_launches += 3;
     return SFC_OK;
 }
@@ -739,6 +743,11 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     cu(dev_alloc(&e->ev, e->cells * 2), "cudaMalloc(event map)");
     cu(dev_alloc(&e->ctl, 1), "cudaMalloc(ctl)");
     cu(dev_alloc(&e->dense_list, k5_tile_count(e->g)), "cudaMalloc(dense tile list)");
+    {
+        const long long words = (rebuild_tile_count(e->g) + 31) / 32;
+        cu(dev_alloc(&e->rebuild_changed, words), "cudaMalloc(rebuild tile bits)");
+        if (rc == SFC_OK) cu(cudaMemset(e->rebuild_changed, 0, sizeof(unsigned) * (size_t)std::max<long long>(words, 1)), "cudaMemset");
+    }
     e->k5_window_ok = e->k5_tile_rows == kMarkTileH && k5_window_supported(e->tabs);
     if (e->k5_tile_rows == kMarkTileH) { // active-tile list: 32 x 8 su tiles over the owned rows
         TileMarks& m = e->marks_alloc;
@@ -826,6 +835,7 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->ev);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
+    cudaFree(e->rebuild_changed);
     stager_destroy(e);
     cudaFree(e->marks_alloc.epoch);
     cudaFree(e->marks_alloc.list);

@@ -317,7 +317,10 @@ long long k5_tile_count(const GridDev& g);
 // mode 1: compare with dyn and record the per-kind drift maxima in ctl; mode 2: overwrite dyn
 // unless ctl holds an error.
 cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
-                           float* dyn, float* out, Ctl* ctl, int mode, double tolerance);
+                           float* dyn, float* out, Ctl* ctl, int mode, double tolerance, unsigned* changed = nullptr);
+// `changed`: one bit per rebuild tile (rebuild_tile_count(g) bits).  Mode 1 sets the bit of every tile where a fresh value
+// differs from the image bit for bit; mode 2 then skips the tiles whose bit is clear and clears the others' (nullptr: every tile).
+long long rebuild_tile_count(const GridDev& g);
 cudaError_t launch_drift_verdict(cudaStream_t s, Ctl* ctl, double tolerance);
 
 // debug materialisation of the reference's temporaries

@@ -36,6 +36,7 @@ struct RbArgs {
     int tiles_x;
     int mode;
     int cap; // power of two
+    unsigned* changed; // one bit per tile, or nullptr (see launch_rebuild)
 };
 
 __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
@@ -48,6 +49,10 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     const GridDev g = a.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (a.mode == 2 && a.ctl->error_code != 0) return;
+    if (a.mode == 2 && a.changed != nullptr) { // the check pass found this tile's images equal to the fresh ones, bit for bit
+        const unsigned word = a.changed[blockIdx.x >> 5], bit = 1u << (blockIdx.x & 31);
+        if (!(word & bit)) return; // (uniform)
+    }
 
     const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
     const int x0 = tile_x * kTileW, y0 = g.row0 + tile_y * kRbTileH;
@@ -150,6 +155,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     }
 
     float drift[kKinds] = {0.0f, 0.0f, 0.0f};
+    bool differs = false;
     if (active) { // the su's 96-byte record as six 16-byte accesses
         const long long cell = cell_index(g, x0 + lx, y0 + ly);
         float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + cell * 24);
@@ -163,8 +169,10 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int q = 4 * v + c;
-                    const float d = fabsf(o[c] - acc[q * kRbThreads + tid]);
+                    const float fresh = acc[q * kRbThreads + tid];
+                    const float d = fabsf(o[c] - fresh);
                     if (drift[q / 8] < d) drift[q / 8] = d; // std::max(worst, d): a NaN never wins
+                    differs = differs || __float_as_uint(o[c]) != __float_as_uint(fresh);
                 }
             }
         } else {
@@ -172,6 +180,14 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
             for (int v = 0; v < 6; ++v)
                 rec[v] = make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
                                      acc[(4 * v + 2) * kRbThreads + tid], acc[(4 * v + 3) * kRbThreads + tid]);
+        }
+    }
+    if (a.changed != nullptr) { // the tile's "commit needed" bit: set by the check pass, consumed by the commit pass
+        if (a.mode == 1) {
+            if (__any_sync(0xFFFFFFFFu, differs) && lane == 0) atomicOr(&a.changed[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
+        } else if (a.mode == 2) {
+            __syncthreads(); // (every thread of the CTA has read the word)
+            if (tid == 0) atomicAnd(&a.changed[blockIdx.x >> 5], ~(1u << (blockIdx.x & 31)));
         }
     }
     if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
@@ -254,8 +270,10 @@ cudaError_t prepare_rebuild(const TablesDev& t) {
     return grant.raise(reinterpret_cast<const void*>(rebuild_kernel), rebuild_smem(t), 48 * 1024);
 }
 
+long long rebuild_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + kRbTileH - 1) / kRbTileH); }
+
 cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
-                           float* dyn, float* out, Ctl* ctl, int mode, double /*tolerance*/) {
+                           float* dyn, float* out, Ctl* ctl, int mode, double /*tolerance*/, unsigned* changed) {
     RbArgs a;
     a.g = g;
     a.t = t;
@@ -265,6 +283,7 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     a.out = out;
     a.ctl = ctl;
     a.mode = mode;
+    a.changed = changed;
     a.tiles_x = (g.W + kTileW - 1) / kTileW;
     a.cap = rebuild_cap(t);
     if (const char* knob = std::getenv("SFC_REBUILD_CAP")) // (tests: a short sorted list forces the id-range rounds)
