@@ -100,6 +100,9 @@ struct sfc_engine {
     int pairs_red_tables = 0; // ... as far as the field magnitudes go (all >= 2^-40: sums are multiples of 2^-115)
     int pairs_red_pref = -1;  // SFC_K5_RED: 0 never, 1 always (tests), -1 when provably exact
     int negative_zero = 0;    // the uploaded images held a -0.0f (Ctl::negative_zero): runs end with the normalising pass
+    double move_rate = 1.0;   // mean over the population of 1 / walk_period (upload)
+    double events_per_window = 0.0; // movement events a field window sees per tick: estimated at upload, measured after every run
+    int k5_crowded = 0;       // crowds: the per-position list walk beats the per-event pair kernel (select_k5_path)
     FieldTables field{};      // tables of the large-field kernel (blob == nullptr: not available for these tables)
     int k5_field = 0;         // the large-field kernel is the k-5 kernel (chosen in sfc_upload)
     int field_ctas[2] = {148, 148}; // its persistent grids ([1]: the lazy shape)
@@ -515,15 +518,24 @@ int upload_peds(sfc_engine* e, const sfc_state_view* v, std::vector<int2>* gate,
     gate->resize((size_t)P);
     attr->resize((size_t)P);
     int max_hh = 0;
+    double rate = 0.0;
     for (long long i = 0; i < P; ++i) {
         const int hw = (v->foot_w[i] - 1) / 2, hh = (v->foot_h[i] - 1) / 2;
         if (hw > kMaxHalfExtent || hh > kMaxHalfExtent || hw < 0 || hh < 0)
             return fail(e, SFC_E_CONFIG, "footprint: pedestrian footprint exceeds the device limit (4095)");
         max_hh = std::max(max_hh, hh);
+        rate += 1.0 / (double)std::max(1, v->walk_period[i]);
         (*gate)[(size_t)i] = make_int2(v->walk_period[i], v->walk_phase[i]);
         (*attr)[(size_t)i] = pack_attr(v->goal_sect[i] & 7, v->orient_attractive[i] & 7, v->orient_repulsive[i] & 7, hw, hh);
     }
     *max_hh_out = max_hh;
+    e->move_rate = P > 0 ? rate / (double)P : 1.0;
+    {   // movers per tick before anything has been measured: everybody whose gate is open, less the share a crowd blocks
+        const double cells = std::max(1.0, (double)e->g.W * (double)e->g.H), rho = (double)P / cells;
+        const double movers = (double)P * e->move_rate * std::min(1.0, 1.3 * std::max(0.0, 1.0 - rho));
+        e->events_per_window = 2.0 * movers * (double)(e->walk.n + 1) / cells;
+        e->k5_crowded = e->events_per_window > 16.0;
+    }
     if (P > 0) {
         SFC_CUDA(cudaMemcpyAsync(e->peds.center, v->center_xy, sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
         SFC_CUDA(cudaMemcpyAsync(e->peds.gate, gate->data(), sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
@@ -553,7 +565,10 @@ int select_k5_path(sfc_engine* e, long long P, bool allow_list) {
         //                                   below the scatter kernel's from corridor densities up, far below for crowds
         //   else                         -> scatter kernel (+ list walk or event-walk gather for dense tiles)
         //   fields beyond 15 x 15        -> the large-field kernel (every tile; sparse crowds: the window kernel)
-        const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || e->k5_path_pref < 0);
+        //   crowds on small fields       -> the list walk again: its cost per su is flat, the pair kernel's grows with the
+        //                                   events (measured cross-over: 16 events per 7 x 7 window, profiles/k5_crossover.py)
+        const bool walk_ok = e->k5_listwalk && k5_listwalk_supported(e->walk) && e->walk.n <= 128;
+        const int pairs = e->pairs.blob != nullptr && (e->k5_path_pref == 3 || (e->k5_path_pref < 0 && !(e->k5_crowded && walk_ok)));
         const int window = allow_list && !pairs && e->k5_window_ok && (e->k5_path_pref == 1 || (e->k5_path_pref < 0 && sparse));
         const int field = !pairs && !window && e->field.blob != nullptr &&
                           (e->k5_path_pref == 4 || (e->k5_path_pref < 0 && e->walk.n > 224));
@@ -1075,10 +1090,23 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
         SFC_CUDA(cudaMemcpyAsync(moved.data(), e->moved_counts, sizeof(unsigned long long) * (size_t)ticks,
                                  cudaMemcpyDeviceToHost, e->stream));
     }
+    unsigned long long last_moved = 0;
+    SFC_CUDA(cudaMemcpyAsync(&last_moved, e->moved_counts + (ticks - 1), sizeof last_moved, cudaMemcpyDeviceToHost, e->stream));
     rc = check_device_error(e); // synchronises
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
     e->last_run_ms = ms;
+    if (rc == SFC_OK && !e->slab.active && e->k5_path_pref < 0) {
+        // The crowd tells which small-field kernel suits it: re-choose between runs from the movers of the last tick
+        // (with hysteresis around the measured cross-over; both kernels give the same bits).
+        e->events_per_window = 2.0 * (double)last_moved * (double)(e->walk.n + 1) / std::max(1.0, (double)e->g.W * (double)e->g.H);
+        const int crowded = e->k5_crowded ? e->events_per_window > 13.0 : e->events_per_window > 19.0;
+        if (crowded != e->k5_crowded) {
+            e->k5_crowded = crowded;
+            const int rc2 = select_k5_path(e, e->peds.n, true);
+            if (rc2 != SFC_OK) return rc2;
+        }
+    }
     if (metrics) {
         for (long long t = 0; t < ticks; ++t) {
             sfc_tick_metrics& m = metrics[t];
