@@ -534,7 +534,7 @@ int upload_peds(sfc_engine* e, const sfc_state_view* v, std::vector<int2>* gate,
         const double cells = std::max(1.0, (double)e->g.W * (double)e->g.H), rho = (double)P / cells;
         const double movers = (double)P * e->move_rate * std::min(1.0, 1.3 * std::max(0.0, 1.0 - rho));
         e->events_per_window = 2.0 * movers * (double)(e->walk.n + 1) / cells;
-        e->k5_crowded = e->events_per_window > 16.0;
+        e->k5_crowded = e->events_per_window > (double)(e->walk.n + 1) / 3.0; // (measured: 16 events per 7 x 7 window)
     }
     if (P > 0) {
         SFC_CUDA(cudaMemcpyAsync(e->peds.center, v->center_xy, sizeof(int2) * (size_t)P, cudaMemcpyHostToDevice, e->stream));
@@ -1100,7 +1100,8 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
         // The crowd tells which small-field kernel suits it: re-choose between runs from the movers of the last tick
         // (with hysteresis around the measured cross-over; both kernels give the same bits).
         e->events_per_window = 2.0 * (double)last_moved * (double)(e->walk.n + 1) / std::max(1.0, (double)e->g.W * (double)e->g.H);
-        const int crowded = e->k5_crowded ? e->events_per_window > 13.0 : e->events_per_window > 19.0;
+        const double cross = (double)(e->walk.n + 1) / 3.0; // the walk's cost grows with the positions, the pairs' with the events
+        const int crowded = e->k5_crowded ? e->events_per_window > 0.8 * cross : e->events_per_window > 1.2 * cross;
         if (crowded != e->k5_crowded) {
             e->k5_crowded = crowded;
             const int rc2 = select_k5_path(e, e->peds.n, true);

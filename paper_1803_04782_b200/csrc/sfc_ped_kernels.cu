@@ -291,8 +291,12 @@ __device__ __forceinline__ int wrapped_intervals(int lo, int hi, int n, bool clo
 }
 
 // Lists every k-5 tile within field reach of a mover's old or new centre (TileMarks).
+constexpr int kFirstsMax = 4; // tiles one mover can be the first to stamp before it appends them itself (7 x 7 fields: at most 2 x 2)
+
+// `firsts` / `n_firsts`: tiles this mover stamped first this tick; the caller appends them to the list with one
+// atomic per WARP (every first of a tick bumps the same counter).
 __device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m, Ctl* ctl, unsigned epoch, int fx, int fy, int ux,
-                                           int uy, bool slab_active) {
+                                           int uy, bool slab_active, int (&firsts)[kFirstsMax], int& n_firsts) {
     int xr[2][2], yr[2][2];
     const int nxr = wrapped_intervals(min(fx, fx + ux) - m.hw, max(fx, fx + ux) + m.hw, g.W, g.closed != 0, 0, g.W, xr);
     const int nyr = wrapped_intervals(min(fy, fy + uy) - m.hh, max(fy, fy + uy) + m.hh, g.H, g.closed != 0, g.row0, g.rows, yr);
@@ -318,7 +322,10 @@ __device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m,
                         const unsigned b = (current ? (old >> 8) & 0xFFu : 0u) | blocks;
                         const unsigned prev = atomicCAS(m.epoch + t, old, (epoch << 16) | (b << 8) | n);
                         if (prev == old) {
-                            if (!current) m.list[atomicAdd(&ctl->active_count, 1)] = t;
+                            if (!current) {
+                                if (n_firsts < kFirstsMax) firsts[n_firsts++] = t;
+                                else m.list[atomicAdd(&ctl->active_count, 1)] = t; // (large fields: more tiles than the buffer holds)
+                            }
                             break;
                         }
                         old = prev;
@@ -332,6 +339,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
                unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab, TileMarks marks) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool moved = false;
+    int firsts[kFirstsMax], n_firsts = 0;
     if (i == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
     if (i < p.n && ctl->error_code == 0) {
         const int d = p.dir[i];
@@ -372,7 +380,7 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             if (from >= 0) ev[2 * from] = code;
             if (to >= 0) ev[2 * to + 1] = code;
             p.moved_dir[i] = (int8_t)d;
-            if (marks.epoch) mark_tiles(g, marks, ctl, ctl->epoch, c.x, c.y, ux, uy, slab.active != 0);
+            if (marks.epoch) mark_tiles(g, marks, ctl, ctl->epoch, c.x, c.y, ux, uy, slab.active != 0, firsts, n_firsts);
             if (slab.band) {
                 p.won[i] = 0;
             } else if (slab.active) { // remember the event cells for next tick's clear
@@ -395,6 +403,23 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
             }
             moved = row_owned(g, c.y); // a neighbour's pedestrian is counted by its owner
         }
+    }
+    // tiles stamped first by this warp's movers go on the active-tile list with one counter bump per warp
+    if (marks.epoch != nullptr && __any_sync(0xFFFFFFFFu, n_firsts != 0)) {
+        const int lane = threadIdx.x & 31;
+        int incl = n_firsts;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int up = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += up;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        int base = 0;
+        if (lane == 31) base = atomicAdd(&ctl->active_count, total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - n_firsts;
+#pragma unroll
+        for (int q = 0; q < kFirstsMax; ++q)
+            if (q < n_firsts) marks.list[base + q] = firsts[q];
     }
     // TickMetrics::moved: one atomic per warp
     const unsigned ballot = __ballot_sync(0xFFFFFFFFu, moved);
