@@ -1681,6 +1681,8 @@ int sfc_band_run(sfc_engine* e, sfc_state_view* v, int64_t ticks, sfc_tick_metri
             status = band_load(e, v, kBandEv, false);
             if (status == SFC_OK) status = band_load(e, v, kBandDyn, true);
             if (status != SFC_OK) break;
+            // (k-4 empties the scatter kernel's hand-off list once per tick; here every band is a k-5 launch of its own)
+            SFC_CUDA(cudaMemsetAsync(&e->ctl->dense_count, 0, sizeof(int), e->stream));
             SFC_CUDA(launch_k5_writeback(e->stream, k5_args(e, 0)));
             e->counters.kernel_launches += e->k5_launches;
             status = band_store(e, v, kBandDyn, true);

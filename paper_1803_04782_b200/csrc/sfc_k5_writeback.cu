@@ -151,7 +151,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
         const bool narrow = RW <= g.W; // one conditional add wraps x (wider regions take the general path)
         { // row-major over the chunk (coalesced), eight loads of a thread in flight before the first use
             const int n_cells = ncols * RH;
-            const unsigned inv_cols = 0xFFFFFFFFu / (unsigned)ncols + 1u;
+            const unsigned inv_cols = ncols > 1 ? 0xFFFFFFFFu / (unsigned)ncols + 1u : 0u; // (a one-column chunk: the reciprocal would wrap to 0)
             for (int i0 = 0; i0 < n_cells; i0 += 8 * NT) {
                 uint16_t got[8];
                 int at[8];
@@ -161,7 +161,7 @@ __device__ void process_tile(const K5Args& a, const Smem& sm, const int tile) {
                     got[q] = 0;
                     at[q] = -1;
                     if (i < n_cells) {
-                        const int ry = (int)__umulhi((unsigned)i, inv_cols); // i / ncols
+                        const int ry = ncols > 1 ? (int)__umulhi((unsigned)i, inv_cols) : i; // i / ncols
                         const int rc = i - ry * ncols;
                         at[q] = rc * RH + ry;
                         int x = xs + c0 + rc;

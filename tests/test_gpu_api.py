@@ -462,7 +462,8 @@ def test_one_run_across_the_stamp_period(monkeypatch):
 
 
 @pytest.mark.parametrize("name,bands", [("desk64", 2), ("desk64", 3), ("closed-four", 2), ("linear-regulation", 2), ("wide-ragged", 3),
-                                        ("field21", 2), ("ped5", 2), ("k16", 2), ("field35", 2), ("d0.9-eight-ped1", 4)])
+                                        ("field21", 2), ("ped5", 2), ("k16", 2), ("field35", 2), ("d0.9-eight-ped1", 4),
+                                        ("field13-crowd", 2)])  # (13 x 13 in a crowd: scatter kernel handing tiles to the dense kernel, per band)
 def test_band_swapped_pass_equals_undivided_grid(product_lib, monkeypatch, name, bands):
     """A state larger than device memory streams through the device in row bands, the host SimState
     being the backing store (sfc_band_run: the paper's divide-and-conquer as a band pass; reference
