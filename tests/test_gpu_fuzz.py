@@ -16,10 +16,12 @@ pytestmark = pytest.mark.gpu
 
 def random_scenario(rng: random.Random):
     closed = rng.random() < 0.3
-    fw, fh = rng.choice([(3, 3), (5, 5), (7, 7), (9, 9), (5, 9), (11, 7), (13, 13), (17, 15), (21, 21), (25, 31), (37, 37), (45, 29)])
+    fw, fh = rng.choice([(3, 3), (5, 5), (7, 7), (9, 9), (5, 9), (11, 7), (13, 13), (17, 15), (21, 21), (25, 31), (37, 37), (45, 29),
+                         (7, 7), (7, 7), (61, 45), (77, 77), (9, 5), (15, 15), (19, 41)])
     pw, ph = rng.choice([(1, 1)] * 5 + [(3, 3), (3, 1), (1, 3), (5, 3)])
-    w = rng.randint(max(6, pw + 2), 150)
-    h = rng.randint(max(6, ph + 2), 110)
+    big = rng.random() < 0.15
+    w = rng.randint(max(6, pw + 2), 260 if big else 150)
+    h = rng.randint(max(6, ph + 2), 190 if big else 110)
     area = pw * ph
     density = rng.choice([0.002, 0.01, 0.05, 0.15, 0.3, 0.5, 0.8]) / (1 if area == 1 else 1.6)
     lines = [f"grid = {w}x{h}", f"density = {density}", f"directions = {rng.choice(['uni', 'bi', 'four', 'eight'])}",
