@@ -64,8 +64,13 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     const bool active = lx < nx && ly < ny;
     const int tcx = lx + HW, tcy = ly + HH;
 
+    bool have_acc = false; // (most tiles of a sparse crowd see no centre: their sums are never materialised)
+    // check pass: the su's record is requested now and compared after the region has been scanned and summed
+    const long long my_cell = active ? cell_index(g, x0 + lx, y0 + ly) : 0;
+    float4 old[6];
 #pragma unroll
-    for (int q = 0; q < kKinds * kSects; ++q) acc[q * kRbThreads + tid] = 0.0f;
+    for (int v = 0; v < 6; ++v)
+        old[v] = (active && a.mode == 1) ? reinterpret_cast<const float4*>(a.dyn + my_cell * 24)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
 
     // The centres of the region are taken in ROUNDS of ascending id ranges: one round over every id when
     // they fit the sorted list (the usual case), else as many equal id ranges as bring a range's expected
@@ -131,6 +136,11 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
             }
         }
 
+        if (n > 0 && !have_acc) { // (a thread's sums are its own column: no barrier needed)
+#pragma unroll
+            for (int q = 0; q < kKinds * kSects; ++q) acc[q * kRbThreads + tid] = 0.0f;
+            have_acc = true;
+        }
         if (active && n > 0) {
             for (int e = 0; e < n; ++e) {
                 const unsigned long long key = keys[e];
@@ -157,19 +167,15 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     float drift[kKinds] = {0.0f, 0.0f, 0.0f};
     bool differs = false;
     if (active) { // the su's 96-byte record as six 16-byte accesses
-        const long long cell = cell_index(g, x0 + lx, y0 + ly);
-        float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + cell * 24);
+        float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + my_cell * 24);
         if (a.mode == 1) {
-            float4 old[6];
-#pragma unroll
-            for (int v = 0; v < 6; ++v) old[v] = rec[v];
 #pragma unroll
             for (int v = 0; v < 6; ++v) {
                 const float o[4] = {old[v].x, old[v].y, old[v].z, old[v].w};
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int q = 4 * v + c;
-                    const float fresh = acc[q * kRbThreads + tid];
+                    const float fresh = have_acc ? acc[q * kRbThreads + tid] : 0.0f;
                     const float d = fabsf(o[c] - fresh);
                     if (drift[q / 8] < d) drift[q / 8] = d; // std::max(worst, d): a NaN never wins
                     differs = differs || __float_as_uint(o[c]) != __float_as_uint(fresh);
@@ -178,8 +184,9 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         } else {
 #pragma unroll
             for (int v = 0; v < 6; ++v)
-                rec[v] = make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
-                                     acc[(4 * v + 2) * kRbThreads + tid], acc[(4 * v + 3) * kRbThreads + tid]);
+                rec[v] = have_acc ? make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
+                                                acc[(4 * v + 2) * kRbThreads + tid], acc[(4 * v + 3) * kRbThreads + tid])
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     if (a.changed != nullptr) { // the tile's "commit needed" bit: set by the check pass, consumed by the commit pass
