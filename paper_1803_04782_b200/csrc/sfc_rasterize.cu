@@ -76,33 +76,50 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     // they fit the sorted list (the usual case), else as many equal id ranges as bring a range's expected
     // share under half the capacity — per-address order is ascending id either way, so the float sums are
     // the reference's.  (Ids are handed out in placement order, i.e. uniformly over the grid.)
-    const int ncell = RW * RH;
     int rounds = 1;
     for (int round = 0; round < rounds; ++round) {
         const long long id_lo = rounds == 1 ? 0 : a.p.n * round / rounds, id_hi = rounds == 1 ? a.p.n : a.p.n * (round + 1) / rounds;
         __syncthreads(); // (the previous round's walk is done with the keys)
         if (tid == 0) s_count = 0;
-        for (int i = tid; i < a.cap; i += kRbThreads) keys[i] = ~0ull;
         __syncthreads();
-        // collect the pedestrian centres of the region (any order; sorted below)
-        for (int i = tid; i < ncell; i += kRbThreads) {
-            const int ryi = i / RW, rxi = i - ryi * RW;
-            const long long idx = cell_index(g, xs + rxi, ys + ryi);
-            if (idx < 0) continue;
-            const int id = a.occ[idx];
-            if (id < id_lo || id >= id_hi) continue; // (empty su hold -1)
-            const int2 c = a.p.center[id];
-            int wx = xs + rxi, wy = ys + ryi;
-            if (!g.closed) {
-                wx = emod(wx, g.W);
-                wy = emod(wy, g.H);
-            }
-            if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
-            const int pos = atomicAdd(&s_count, 1);
-            if (pos < a.cap) {
-                const uint32_t attr = a.p.attr[id];
-                keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
-                            ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+        // collect the pedestrian centres of the region (any order; sorted below); (row, column) of a thread's cells
+        // advance incrementally — no division, one wrap per axis
+        const bool narrow = RW <= g.W; // (a field wider than the grid wraps more than once: the general path)
+        {
+            const int dr = kRbThreads / RW, dc = kRbThreads - dr * RW;
+            int ryi = tid / RW, rxi = tid - ryi * RW;
+            for (; ryi < RH; rxi += dc, ryi += dr) {
+                if (rxi >= RW) {
+                    rxi -= RW;
+                    if (++ryi >= RH) break;
+                }
+                int wx = xs + rxi, wy = ys + ryi;
+                long long idx;
+                if (narrow) {
+                    const long long row = cell_index(g, 0, wy); // -1: the row does not exist / is not resident
+                    if (row < 0) continue;
+                    if (g.closed) {
+                        if (wx < 0 || wx >= g.W) continue;
+                    } else {
+                        wx += wx < 0 ? g.W : (wx >= g.W ? -g.W : 0);
+                    }
+                    idx = row + wx;
+                } else {
+                    idx = cell_index(g, wx, wy);
+                    if (idx < 0) continue;
+                    if (!g.closed) wx = emod(wx, g.W);
+                }
+                if (!g.closed) wy = emod(wy, g.H);
+                const int id = a.occ[idx];
+                if (id < id_lo || id >= id_hi) continue; // (empty su hold -1)
+                const int2 c = a.p.center[id];
+                if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
+                const int pos = atomicAdd(&s_count, 1);
+                if (pos < a.cap) {
+                    const uint32_t attr = a.p.attr[id];
+                    keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
+                                ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+                }
             }
         }
         __syncthreads();
@@ -119,6 +136,10 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         // bitonic sort of the first pow2 >= n keys (padding keys are all-ones)
         int m = 1;
         while (m < n) m <<= 1;
+        if (m > n) {
+            for (int i = n + tid; i < m; i += kRbThreads) keys[i] = ~0ull;
+            __syncthreads();
+        }
         for (int k = 2; k <= m; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
                 for (int i = tid; i < m; i += kRbThreads) {
@@ -168,7 +189,15 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     bool differs = false;
     if (active) { // the su's 96-byte record as six 16-byte accesses
         float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + my_cell * 24);
-        if (a.mode == 1) {
+        bool blank = false; // nothing in reach and the record is all +0.0f: equal, no drift
+        if (a.mode == 1 && !have_acc) {
+            uint32_t any_bits = 0u;
+#pragma unroll
+            for (int v = 0; v < 6; ++v)
+                any_bits |= __float_as_uint(old[v].x) | __float_as_uint(old[v].y) | __float_as_uint(old[v].z) | __float_as_uint(old[v].w);
+            blank = any_bits == 0u;
+        }
+        if (a.mode == 1 && !blank) {
 #pragma unroll
             for (int v = 0; v < 6; ++v) {
                 const float o[4] = {old[v].x, old[v].y, old[v].z, old[v].w};
@@ -181,7 +210,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
                     differs = differs || __float_as_uint(o[c]) != __float_as_uint(fresh);
                 }
             }
-        } else {
+        } else if (a.mode != 1) {
 #pragma unroll
             for (int v = 0; v < 6; ++v)
                 rec[v] = have_acc ? make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
@@ -198,11 +227,14 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         }
     }
     if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
+        const bool some = __any_sync(0xFFFFFFFFu, drift[0] > 0.0f || drift[1] > 0.0f || drift[2] > 0.0f);
 #pragma unroll
         for (int k = 0; k < kKinds; ++k) {
             float v = drift[k];
+            if (some) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+                for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+            }
             if (lane == 0) s_drift[k][warp] = v;
         }
         __syncthreads();
