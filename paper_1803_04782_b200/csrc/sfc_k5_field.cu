@@ -83,7 +83,7 @@ __device__ __forceinline__ uint32_t selector(uint32_t b) { // one-hot orientatio
 
 // ONE_MAG: the kinds of a walk share one magnitude table (always true for NK == 1).
 template <int K, int NK, bool LAZY, bool ONE_MAG>
-__global__ void __launch_bounds__(kMaxThreads) k5_field_kernel(FieldArgs a) {
+__global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(FieldArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int KH = K / 2;                // partials per (kind, group) and lane: the even or the odd slots
     constexpr int KO = kSects * KH * 32;     // partial doubles per kind and warp
@@ -432,8 +432,8 @@ bool field_shape(const FieldTables& t, int chunk_k, int nk_pref, int warps_pref,
     if (t.blob == nullptr) return false;
     // crowds (partials cleared per block): one walk for the three kinds; thin crowds (lazy partials): the
     // small shape, several CTAs per SM, so one CTA's staging overlaps another's walks
-    static const int eager_order[6][2] = {{3, 8}, {1, 16}, {1, 8}, {3, 4}, {1, 4}, {3, 16}};
-    static const int lazy_order[6][2] = {{1, 8}, {1, 4}, {1, 16}, {3, 8}, {3, 4}, {3, 16}};
+    static const int eager_order[5][2] = {{3, 8}, {1, 16}, {1, 8}, {3, 4}, {1, 4}}; // (three kinds never run on 16 warps: launch bounds)
+    static const int lazy_order[5][2] = {{1, 8}, {1, 4}, {1, 16}, {3, 8}, {3, 4}};
     for (const auto& cand : lazy ? lazy_order : eager_order) {
         const int nk = cand[0], warps = cand[1];
         if (nk_pref > 0 && nk != nk_pref) continue;
