@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int KH = K / 2;                // partials per (kind, group) and lane: the even or the odd slots
     constexpr int KO = kSects * KH * 32;     // partial doubles per kind and warp
+#ifndef SFC_FIELD_EV
+#define SFC_FIELD_EV (LAZY ? 2 : 4)
+#endif
+    constexpr int EV = SFC_FIELD_EV;         // events a lane looks up before it folds any of them
     constexpr int PW = NK * KO;              // ... per warp
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
@@ -300,12 +304,12 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
                     const int len = e1 - e0;
                     const int steps = max(__shfl_sync(0xFFFFFFFFu, len, 0), __shfl_sync(0xFFFFFFFFu, len, 16));
 #pragma unroll 1
-                    for (int i = 0; i < steps; i += 2) {
-                        // two events per trip: both table lookups are in flight before either event's partials are touched
-                        FieldEvent fe[2];
-                        uint32_t info[2];
+                    for (int i = 0; i < steps; i += EV) {
+                        // EV events per trip: every table lookup is in flight before any event's partials are touched
+                        FieldEvent fe[EV];
+                        uint32_t info[EV];
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < EV; ++h) {
                             const int e = e0 + i + h;
                             fe[h] = my_list[min(e, a.cap - 1)];
                             const int u = (int)fe[h].y - tcx, v = (int)(fe[h].x >> 17) - tcy;
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
                             info[h] = ok ? (uint32_t)tabp[(int)(fe[h].x >> 17) * FW + (int)fe[h].y] : kNoEntry;
                         }
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < EV; ++h) {
                             if (info[h] == kNoEntry) continue;
                             const int grp = (int)info[h] / K;
                             const uint32_t gate = lut[grp] & fe[h].x & kmask; // byte k non-zero: kind k's term is live
