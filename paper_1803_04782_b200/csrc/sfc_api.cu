@@ -5,6 +5,7 @@
 // There is no CPU path: without a CUDA device sfc_create fails with SFC_E_NO_DEVICE.
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -102,6 +103,9 @@ struct sfc_engine {
     int negative_zero = 0;    // the uploaded images held a -0.0f (Ctl::negative_zero): runs end with the normalising pass
     double move_rate = 1.0;   // mean over the population of 1 / walk_period (upload)
     double events_per_window = 0.0; // movement events a field window sees per tick: estimated at upload, measured after every run
+    int order_pref = -1;      // per-pedestrian kernels visit the pedestrians in position order: SFC_PED_ORDER=1 / 0, -1: by grid size
+    int* order_counts = nullptr; // ordering pass scratch
+    long long order_tick = 0; // tick of the last ordering pass
     int k5_crowded = 0;       // crowds: the per-position list walk beats the per-event pair kernel (select_k5_path)
     FieldTables field{};      // tables of the large-field kernel (blob == nullptr: not available for these tables)
     int k5_field = 0;         // the large-field kernel is the k-5 kernel (chosen in sfc_upload)
@@ -124,6 +128,9 @@ struct sfc_engine {
 
 namespace {
 
+constexpr long long kOrderMinPeds = 4096; // smaller crowds are launch-bound: position order buys nothing
+constexpr long long kOrderMinCells = 1ll << 28;
+constexpr long long kOrderPeriod = 50;    // ticks between ordering passes
 constexpr long long kStageCells = 4ll << 20; // 4 Mi su per staging chunk (128 MiB of one image)
 
 int fail(sfc_engine* e, int code, const std::string& msg) {
@@ -179,6 +186,7 @@ void free_peds(sfc_engine* e) {
     cudaFree(e->peds.score);
     cudaFree(e->peds.won);
     cudaFree(e->peds.moved_dir);
+    cudaFree(e->peds.order);
     e->peds = PedArrays{};
     e->ped_capacity = 0;
 }
@@ -198,8 +206,24 @@ int ensure_peds(sfc_engine* e, long long n) {
     SFC_CUDA(dev_alloc(&e->peds.score, n));
     SFC_CUDA(dev_alloc(&e->peds.won, n));
     SFC_CUDA(dev_alloc(&e->peds.moved_dir, n));
+    // Position order trades the coalesced reads of the per-pedestrian arrays for neighbouring grid reads.  Measured
+    // (profiles/README.md): it pays on grids far beyond the L2 and the TLB reach (config 4: k-2 299 -> 243 us, k-3 129 ->
+    // 90 us) and loses where the grid is L2-resident (paper baseline: k-2 47 -> 62 us), so the size of the grid decides.
+    const bool ordered = e->order_pref >= 0 ? e->order_pref != 0 : e->cells >= kOrderMinCells;
+    if (ordered && n >= (e->order_pref > 0 ? 1 : kOrderMinPeds) && n <= INT_MAX) SFC_CUDA(dev_alloc(&e->peds.order, n));
     e->peds.n = n;
     e->ped_capacity = n;
+    return SFC_OK;
+}
+
+// Re-list the pedestrians by position (PedArrays::order) — see order_pedestrians in sfc_ped_kernels.cu.  Row slabs
+// and bands keep id order: their occupancy holds only their rows.
+int enqueue_order(sfc_engine* e, long long tick) {
+    if (!e->peds.order || e->slab.active || e->slab.band) return SFC_OK;
+    if (!e->order_counts) SFC_CUDA(dev_alloc(&e->order_counts, order_chunks(e->cells)));
+    SFC_CUDA(launch_order_pedestrians(e->stream, e->g, e->peds, e->occ, e->cells, e->order_counts, e->ctl));
+    e->counters.kernel_launches += 3;
+    e->order_tick = tick;
     return SFC_OK;
 }
 
@@ -636,6 +660,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_GRAPH_TICKS")) e->graph_ticks = std::clamp(std::atoi(knob), 1, 64);
+    if (const char* knob = std::getenv("SFC_PED_ORDER")) e->order_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
         const std::string path(knob);
@@ -848,6 +873,7 @@ void sfc_destroy(sfc_engine* e) {
     cudaFree(e->stat);
     cudaFree(e->dyn);
     cudaFree(e->ev);
+    cudaFree(e->order_counts);
     cudaFree(e->ctl);
     cudaFree(e->dense_list);
     cudaFree(e->rebuild_changed);
@@ -952,6 +978,8 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
         SFC_CUDA(launch_occupancy_from_peds(e->stream, e->g, e->peds, e->occ));
         e->counters.kernel_launches += 1;
     }
+    rc = enqueue_order(e, v->tick);
+    if (rc != SFC_OK) return rc;
     int tiny = 0;
     SFC_CUDA(cudaMemcpyAsync(&tiny, &e->ctl->tiny_image, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
     SFC_CUDA(cudaMemcpyAsync(&e->negative_zero, &e->ctl->negative_zero, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
@@ -1076,6 +1104,10 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
         t += done;
         if (interval > 0 && (base + t) % interval == 0) {
             rc = enqueue_rebuild(e);
+            if (rc != SFC_OK) return rc;
+        }
+        if (base + t - e->order_tick >= kOrderPeriod) {
+            rc = enqueue_order(e, base + t);
             if (rc != SFC_OK) return rc;
         }
     }

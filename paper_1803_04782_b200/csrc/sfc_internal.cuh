@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
 #include <vector>
 
 #include "socfield_cuda.h"
@@ -72,6 +73,40 @@ __host__ __device__ __forceinline__ bool row_within(const GridDev& g, int y, int
     return ly >= -depth && ly < g.rows + depth;
 }
 
+// ---- chained launches (programmatic dependent launch) ----------------------------------------
+// A tick is four small-to-medium kernels in a row, hundreds of ticks in a run: the gap between two
+// kernels of a stream (drain, then launch) is a visible share of a tick.  Kernels launched with
+// launch_chained may be scheduled while their predecessor drains: they do whatever needs nothing from it
+// (constant tables into shared memory) and then wait for its writes (chain_wait) before touching anything a
+// kernel produces.  Every kernel launched this way must call chain_wait before its first global access to
+// mutable state; on a plain launch the call does nothing.  chain_release lets the successor be scheduled
+// before this kernel ends; measured (profiles/README.md, chained launches), that only pays for crowds small
+// enough to be latency-bound — config 1: 27.4 -> 24.4 us a tick — and costs 3 to 5 % elsewhere (early CTAs of
+// k-5 crowd k-4's SMs), so only the per-pedestrian kernels of small crowds call it.  SFC_CHAIN=0 launches
+// everything plainly.
+constexpr long long kChainReleasePeds = 4096;
+__device__ __forceinline__ void chain_release(bool on) {
+    if (on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void chain_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool chain_enabled(); // sfc_ped_kernels.cu
+
+template <typename... Params, typename... Args>
+cudaError_t launch_chained(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = chain_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Multi-GPU row slabs: what the per-pedestrian kernels need to know beyond GridDev.
 struct SlabDev {
     int active;               // this engine owns a proper sub-range of rows
@@ -113,6 +148,7 @@ struct PedArrays {
     double* score;
     uint8_t* won;     // k-3 result: wins every newly covered su
     int8_t* moved_dir; // direction moved in the previous tick, -1 none (for event clearing)
+    int* order;        // ids by centre, row-major, as of the last ordering pass (valid while Ctl::order_ok); may be null
 };
 
 struct DecideParams {
@@ -140,6 +176,7 @@ struct Ctl {
     unsigned int epoch;      // k-5: this tick's tile stamp (set by k-3, read by k-4 and k-5; never 0)
     int tiny_image;          // upload: an uploaded dynamic-image value is non-zero below 2^-92 — sums could be
                              // subnormal, so k-5 may not use flush-to-zero float reductions (sfc_k5_pairs.cu)
+    int order_ok;            // PedArrays::order is a permutation of this population's ids
     int negative_zero;       // upload: a dynamic-image value is -0.0f.  The reference's k-5 adds (float)total to EVERY
                              // address once anybody moved (engine.cpp:468,524), which turns -0.0f into +0.0f; k-5 here skips
                              // untouched addresses, so the first moving tick is followed by one normalising pass
@@ -339,6 +376,10 @@ cudaError_t launch_normalize_negative_zero(cudaStream_t s, float* dyn, long long
                                            long long first, long long ticks);
 cudaError_t launch_occupancy_from_peds(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ);
 cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl);
+// PedArrays::order from the occupancy grid of an undivided engine (chunk_counts: order_chunks(cells) ints of scratch)
+long long order_chunks(long long cells);
+cudaError_t launch_order_pedestrians(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, long long cells,
+                                     int* chunk_counts, Ctl* ctl);
 cudaError_t launch_static_anchor(cudaStream_t s, const GridDev& g, const KindTableDev& t, float* stat, int ax, int ay,
                                  int orientation);
 cudaError_t prepare_k5_writeback(int chunk_k, const TablesDev& t);

@@ -94,8 +94,6 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
     constexpr int PW = NK * KO;              // ... per warp
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
-    if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
-    if (a.ctl->error_code != 0) return;
 
     // ---- shared memory ------------------------------------------------------------------------
     double* const part_all = reinterpret_cast<double*>(smem_raw);
@@ -115,6 +113,9 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
         if (tid < kSects) lut[tid] = reinterpret_cast<const uint32_t*>(a.blob + a.tab_bytes + a.mag_bytes)[tid];
     }
     __syncthreads();
+    chain_wait(); // (the tables above are constants of the engine, staged while k-4 drains)
+    if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
+    if (a.ctl->error_code != 0) return;
 
     const GridDev g = a.g;
     const int HW = a.hw, HH = a.hh, FW = a.fw, MS = a.ms, NWORDS = a.nwords, CW = 2 * a.nwords;
@@ -497,15 +498,15 @@ void launch_k(cudaStream_t s, const FieldArgs& a, const FieldShape& sh, bool laz
     const int threads = sh.warps * 32;
     if (sh.nk == 3) {
         if (one_mag) {
-            if (lazy) k5_field_kernel<K, 3, true, true><<<blocks, threads, sh.smem, s>>>(a);
-            else k5_field_kernel<K, 3, false, true><<<blocks, threads, sh.smem, s>>>(a);
+            if (lazy) launch_chained(k5_field_kernel<K, 3, true, true>, dim3(blocks), dim3(threads), sh.smem, s, a);
+            else launch_chained(k5_field_kernel<K, 3, false, true>, dim3(blocks), dim3(threads), sh.smem, s, a);
         } else {
-            if (lazy) k5_field_kernel<K, 3, true, false><<<blocks, threads, sh.smem, s>>>(a);
-            else k5_field_kernel<K, 3, false, false><<<blocks, threads, sh.smem, s>>>(a);
+            if (lazy) launch_chained(k5_field_kernel<K, 3, true, false>, dim3(blocks), dim3(threads), sh.smem, s, a);
+            else launch_chained(k5_field_kernel<K, 3, false, false>, dim3(blocks), dim3(threads), sh.smem, s, a);
         }
     } else {
-        if (lazy) k5_field_kernel<K, 1, true, true><<<blocks, threads, sh.smem, s>>>(a);
-        else k5_field_kernel<K, 1, false, true><<<blocks, threads, sh.smem, s>>>(a);
+        if (lazy) launch_chained(k5_field_kernel<K, 1, true, true>, dim3(blocks), dim3(threads), sh.smem, s, a);
+        else launch_chained(k5_field_kernel<K, 1, false, true>, dim3(blocks), dim3(threads), sh.smem, s, a);
     }
 }
 

@@ -57,8 +57,6 @@ template <int K, bool LIST_SMEM>
 __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!a.from_dense_list && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
-    if (a.ctl->error_code != 0) return;
 
     const int n = a.w.n;
     float* const tot = reinterpret_cast<float*>(smem_raw);                          // [kind * 8 + sect][kThreads]
@@ -76,6 +74,9 @@ __global__ void __launch_bounds__(kThreads) k5_listwalk_kernel(LwArgs a) {
             s_mag[4 * i + 3] = 0.0;
         }
     }
+    chain_wait(); // (the walk list above is a constant of the engine, staged while k-4 drains)
+    if (!a.from_dense_list && a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
+    if (a.ctl->error_code != 0) return;
 
     const GridDev g = a.g;
     const int HW = a.w.hw, HH = a.w.hh;
@@ -291,8 +292,7 @@ cudaError_t launch_one(cudaStream_t stream, const K5Launch& l, bool from_dense_l
     long long blocks = a.n_tiles;
     if (blocks > l.listwalk_ctas) blocks = l.listwalk_ctas;
     if (blocks < 1) blocks = 1;
-    k5_listwalk_kernel<K, true><<<(unsigned)blocks, kThreads, sh.smem, stream>>>(a); // (supported lists always fit: kListSmemMax)
-    return cudaGetLastError();
+    return launch_chained(k5_listwalk_kernel<K, true>, dim3((unsigned)blocks), dim3(kThreads), sh.smem, stream, a); // (supported lists always fit: kListSmemMax)
 }
 
 } // namespace

@@ -102,9 +102,8 @@ template <int PASSES, bool RED>
 __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
-    if (a.ctl->error_code != 0) return;
 
+    // (the tables are constants of the engine: they are staged while k-4 drains)
     const int t_entries = a.fh << a.fw;
     unsigned long long* const sT = reinterpret_cast<unsigned long long*>(smem_raw);
     PairEntry* const sE = reinterpret_cast<PairEntry*>(sT + t_entries);
@@ -116,6 +115,9 @@ __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArg
         for (int i = tid; i < kSects * kGroupBits * 2; i += kThreads) dst[i] = src[i];
     }
     __syncthreads();
+    chain_wait();
+    if (a.advance_tick && blockIdx.x == 0 && tid == 0 && a.ctl->error_code == 0) a.ctl->tick += 1;
+    if (a.ctl->error_code != 0) return;
 
     const GridDev g = a.g;
     const int HW = a.hw, HH = a.hh, RW = a.rw, RH = a.rh;
@@ -432,8 +434,8 @@ cudaError_t prepare_one(size_t smem, int sm_count, int* ctas) { // ctas[0]: plai
 
 template <int PASSES>
 void launch_one(cudaStream_t s, const PairArgs& a, bool red, unsigned blocks, size_t smem) {
-    if (red) k5_pairs_kernel<PASSES, true><<<blocks, kThreads, smem, s>>>(a);
-    else k5_pairs_kernel<PASSES, false><<<blocks, kThreads, smem, s>>>(a);
+    if (red) launch_chained(k5_pairs_kernel<PASSES, true>, dim3(blocks), dim3(kThreads), smem, s, a);
+    else launch_chained(k5_pairs_kernel<PASSES, false>, dim3(blocks), dim3(kThreads), smem, s, a);
 }
 
 cudaError_t prepare_k5_pairs(const PairTables& t, int sm_count, int* ctas) {

@@ -10,6 +10,9 @@
 // the occupancy grid plus the per-pedestrian decision arrays: same result, no per-su
 // temporaries, no atomics, no full-grid clear (the reference's k-1).
 
+#include <climits>
+#include <cstdlib>
+
 #include "sfc_internal.cuh"
 
 namespace sfc {
@@ -47,6 +50,15 @@ __device__ __forceinline__ bool for_new_cells(int cx, int cy, int rw, int rh, in
     return true;
 }
 
+// The pedestrian thread t of a per-pedestrian kernel works on.  Pedestrians are seeded at random su, so in id order
+// every thread of a warp reads its own sectors of the images and of the occupancy grid; PedArrays::order lists
+// the ids by centre in row-major order as of the last ordering pass (order_pedestrians below), which puts
+// neighbours in one warp.  Ids stay the tie-break everywhere (engine.cpp:375-378), so the order a tick visits
+// the pedestrians in cannot change its result.
+__device__ __forceinline__ long long ped_of_thread(const PedArrays& p, const Ctl* ctl, long long t) {
+    return (p.order != nullptr && ctl->order_ok != 0) ? (long long)p.order[t] : t;
+}
+
 // One compare-exchange of the sort network on (score, sect) pairs: keep the better key first —
 // higher score, lower sect on ties (engine.cpp:34-41).
 __device__ __forceinline__ void cex(double& sa, int& ia, double& sb, int& ib) {
@@ -59,12 +71,14 @@ __device__ __forceinline__ void cex(double& sa, int& ia, double& sb, int& ib) {
     ia = ti;
 }
 
-__global__ void __launch_bounds__(kPedThreads)
-k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const float* __restrict__ stat,
-                 const float* __restrict__ dyn, uint8_t* __restrict__ ev, Ctl* ctl, DecideParams dp, SlabDev slab) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
+// (The three per-pedestrian phases are device functions of the thread's index.  Running all three in ONE launch for
+// a crowd of one CTA — CTA barriers instead of launches — was measured and is slower: config 1, 29.1 against 25.4 us a
+// tick; the phases are chains of dependent loads, and four CTAs on four SMs hide them better than one.)
+__device__ __forceinline__ void k2_decide_body(long long t, const GridDev& g, const PedArrays& p, const int* occ, const float* __restrict__ stat,
+                                               const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab) {
+    if (t >= p.n) return;
     if (ctl->error_code != 0) return;
+    const long long i = ped_of_thread(p, ctl, t);
     const int2 c = p.center[i];
     if (!row_owned(g, c.y)) return;
     const uint32_t attr = p.attr[i];
@@ -182,14 +196,22 @@ k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const floa
 }
 
 __global__ void __launch_bounds__(kPedThreads)
-k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault, SlabDev slab) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) { // k-4 rebuilds the active-tile list of k-5 every tick
+k2_decide_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, const float* __restrict__ stat,
+                 const float* __restrict__ dyn, uint8_t* __restrict__ ev, Ctl* ctl, DecideParams dp, SlabDev slab) {
+    chain_release(p.n <= kChainReleasePeds);
+    chain_wait();
+    k2_decide_body((long long)blockIdx.x * blockDim.x + threadIdx.x, g, p, occ, stat, dyn, ev, ctl, dp, slab);
+}
+
+__device__ __forceinline__ void k3_vote_body(long long t, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl, int fault,
+                                             const SlabDev& slab) {
+    if (t == 0) { // k-4 rebuilds the active-tile list of k-5 every tick
         ctl->active_count = 0;
         ctl->epoch = (unsigned)(ctl->tick % kEpochPeriod) + 1u;
     }
-    if (i >= p.n) return;
+    if (t >= p.n) return;
     if (ctl->error_code != 0) return;
+    const long long i = ped_of_thread(p, ctl, t);
     const int d = p.dir[i];
     if (d < 0) return;
     const int2 c = p.center[i];
@@ -335,13 +357,21 @@ __device__ __forceinline__ void mark_tiles(const GridDev& g, const TileMarks& m,
 }
 
 __global__ void __launch_bounds__(kPedThreads)
-k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restrict__ ev, Ctl* ctl,
-               unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab, TileMarks marks) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+k3_vote_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, Ctl* ctl, int fault, SlabDev slab) {
+    chain_release(p.n <= kChainReleasePeds);
+    chain_wait();
+    k3_vote_body((long long)blockIdx.x * blockDim.x + threadIdx.x, g, p, occ, ctl, fault, slab);
+}
+
+// (every thread of the warp comes here, pedestrian or not: the tail is warp-collective)
+__device__ __forceinline__ void k4_move_body(long long t, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
+                                             unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab,
+                                             const TileMarks& marks) {
     bool moved = false;
     int firsts[kFirstsMax], n_firsts = 0;
-    if (i == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
-    if (i < p.n && ctl->error_code == 0) {
+    if (t == 0) ctl->dense_count = 0; // k-5's dense-tile list starts empty every tick
+    if (t < p.n && ctl->error_code == 0) {
+        const long long i = ped_of_thread(p, ctl, t);
         const int d = p.dir[i];
         const int2 c = p.center[i];
         if (d >= 0 && p.won[i] && row_within(g, c.y, slab.reach)) {
@@ -426,6 +456,14 @@ k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restric
     if ((threadIdx.x & 31) == 0 && ballot != 0) {
         atomicAdd(&moved_counts[ctl->tick - ctl->run_base], (unsigned long long)__popc(ballot));
     }
+}
+
+__global__ void __launch_bounds__(kPedThreads)
+k4_move_kernel(GridDev g, PedArrays p, int* __restrict__ occ, uint8_t* __restrict__ ev, Ctl* ctl,
+               unsigned long long* __restrict__ moved_counts, DebugArrays dbg, SlabDev slab, TileMarks marks) {
+    chain_release(p.n <= kChainReleasePeds);
+    chain_wait();
+    k4_move_body((long long)blockIdx.x * blockDim.x + threadIdx.x, g, p, occ, ev, ctl, moved_counts, dbg, slab, marks);
 }
 
 // ---- reference-shaped temporaries for the Inspector path -----------------------------------
@@ -570,25 +608,105 @@ inline unsigned blocks_for(long long n, int threads) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
+// ---- ordering pass: PedArrays::order = ids by centre, row-major ------------------------------
+// The occupancy grid already is the pedestrians sorted by position: a compaction of the su that hold a centre,
+// taken in flat order, is the list.  Three launches (count per chunk, scan, write), run at upload and every
+// kOrderPeriod ticks — pedestrians move one su per tick, so the order stays nearly sorted in between.
+constexpr int kOrdThreads = 256;
+constexpr int kOrdChunk = 4096; // su per block
+
+__device__ __forceinline__ bool centre_at(const GridDev& g, const PedArrays& p, const int* __restrict__ occ, long long su,
+                                          long long cells, int& id) {
+    id = su < cells ? occ[su] : kNoPed;
+    if (id < 0) return false;
+    const int2 c = p.center[id];
+    return cell_index(g, c.x, c.y) == su; // (a footprint's other su carry the id too)
+}
+
+__global__ void __launch_bounds__(kOrdThreads)
+order_count_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, long long cells, int* __restrict__ counts) {
+    __shared__ int warp_n[kOrdThreads / 32];
+    const long long base = (long long)blockIdx.x * kOrdChunk;
+    int n = 0, id;
+#pragma unroll 4
+    for (int r = 0; r < kOrdChunk / kOrdThreads; ++r) n += centre_at(g, p, occ, base + r * kOrdThreads + threadIdx.x, cells, id) ? 1 : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) n += __shfl_xor_sync(0xFFFFFFFFu, n, d);
+    if ((threadIdx.x & 31) == 0) warp_n[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int total = 0;
+        for (int w = 0; w < kOrdThreads / 32; ++w) total += warp_n[w];
+        counts[blockIdx.x] = total;
+    }
+}
+
+// counts -> exclusive starts, in place (one CTA); the list is used only if it holds every pedestrian exactly once
+__global__ void __launch_bounds__(1024) order_scan_kernel(int* __restrict__ counts, long long n_chunks, long long population, Ctl* ctl) {
+    __shared__ long long part[1024];
+    const long long per = (n_chunks + 1023) / 1024;
+    const long long lo = min(n_chunks, threadIdx.x * per), hi = min(n_chunks, lo + per);
+    long long sum = 0;
+    for (long long i = lo; i < hi; ++i) sum += counts[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+        const long long v = (int)threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    long long run = part[threadIdx.x] - sum;
+    for (long long i = lo; i < hi; ++i) {
+        const int c = counts[i];
+        counts[i] = (int)min(run, (long long)INT_MAX);
+        run += c;
+    }
+    if (threadIdx.x == 1023) ctl->order_ok = part[1023] == population ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kOrdThreads)
+order_write_kernel(GridDev g, PedArrays p, const int* __restrict__ occ, long long cells, const int* __restrict__ starts,
+                   const Ctl* ctl) {
+    __shared__ int warp_n[2][kOrdThreads / 32];
+    if (ctl->order_ok == 0) return;
+    const long long base = (long long)blockIdx.x * kOrdChunk;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int run = starts[blockIdx.x];
+    for (int r = 0; r < kOrdChunk / kOrdThreads; ++r) {
+        int id;
+        const bool here = centre_at(g, p, occ, base + r * kOrdThreads + threadIdx.x, cells, id);
+        const unsigned ballot = __ballot_sync(0xFFFFFFFFu, here);
+        if (lane == 0) warp_n[r & 1][warp] = __popc(ballot);
+        __syncthreads(); // (double-buffered counts: one barrier per round)
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kOrdThreads / 32; ++w) {
+            const int c = warp_n[r & 1][w];
+            before += w < warp ? c : 0;
+            total += c;
+        }
+        if (here) p.order[run + before + __popc(ballot & ((1u << lane) - 1u))] = id;
+        run += total;
+    }
+}
+
 } // namespace
 
 cudaError_t launch_k2_decide(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, const float* stat,
                              const float* dyn, uint8_t* ev, Ctl* ctl, const DecideParams& dp, const SlabDev& slab) {
-    k2_decide_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, stat, dyn, ev, ctl, dp, slab);
-    return cudaGetLastError();
+    return launch_chained(k2_decide_kernel, dim3(blocks_for(p.n, kPedThreads)), dim3(kPedThreads), 0, s, g, p, occ, stat, dyn, ev, ctl, dp, slab);
 }
 
 cudaError_t launch_k3_vote(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, Ctl* ctl,
                            const DecideParams& dp, const SlabDev& slab) {
-    k3_vote_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ctl, dp.fault_invert, slab);
-    return cudaGetLastError();
+    return launch_chained(k3_vote_kernel, dim3(blocks_for(p.n, kPedThreads)), dim3(kPedThreads), 0, s, g, p, occ, ctl, dp.fault_invert, slab);
 }
 
 cudaError_t launch_k4_move(cudaStream_t s, const GridDev& g, const PedArrays& p, int* occ, uint8_t* ev, Ctl* ctl,
                            unsigned long long* moved_counts, const DebugArrays& dbg, const SlabDev& slab,
                            const TileMarks& marks) {
-    k4_move_kernel<<<blocks_for(p.n, kPedThreads), kPedThreads, 0, s>>>(g, p, occ, ev, ctl, moved_counts, dbg, slab, marks);
-    return cudaGetLastError();
+    return launch_chained(k4_move_kernel, dim3(blocks_for(p.n, kPedThreads)), dim3(kPedThreads), 0, s, g, p, occ, ev, ctl, moved_counts, dbg, slab, marks);
 }
 
 cudaError_t launch_dbg_clear(cudaStream_t s, const DebugArrays& d) {
@@ -639,6 +757,26 @@ cudaError_t launch_normalize_negative_zero(cudaStream_t s, float* dyn, long long
 
 cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl) {
     tick_advance_kernel<<<1, 1, 0, s>>>(ctl);
+    return cudaGetLastError();
+}
+
+bool chain_enabled() {
+    static const bool on = [] {
+        const char* knob = std::getenv("SFC_CHAIN");
+        return knob == nullptr || std::atoi(knob) != 0;
+    }();
+    return on;
+}
+
+long long order_chunks(long long cells) { return (cells + kOrdChunk - 1) / kOrdChunk; }
+
+cudaError_t launch_order_pedestrians(cudaStream_t s, const GridDev& g, const PedArrays& p, const int* occ, long long cells,
+                                     int* chunk_counts, Ctl* ctl) {
+    const long long n_chunks = order_chunks(cells);
+    if (n_chunks == 0 || p.order == nullptr) return cudaSuccess;
+    order_count_kernel<<<(unsigned)n_chunks, kOrdThreads, 0, s>>>(g, p, occ, cells, chunk_counts);
+    order_scan_kernel<<<1, 1024, 0, s>>>(chunk_counts, n_chunks, p.n, ctl);
+    order_write_kernel<<<(unsigned)n_chunks, kOrdThreads, 0, s>>>(g, p, occ, cells, chunk_counts, ctl);
     return cudaGetLastError();
 }
 

@@ -336,6 +336,21 @@ def test_field_kernel(product_lib, monkeypatch, name, nk, warps, lazy, cap):
         assert_state_equal(gpu, cpu, f"{name} nk {nk} warps {warps} lazy {lazy} cap {cap} tick {ticks * (step + 1)}")
 
 
+@pytest.mark.parametrize("name", ["desk64", "closed-ped3", "d0.9-eight-ped1", "linear-regulation", "sparse-periodic", "wide-ragged"])
+def test_position_ordered_pedestrian_kernels(product_lib, monkeypatch, name):
+    """k-2 ... k-4 visiting the pedestrians in row-major order of their centres (PedArrays::order, the engine's
+    choice on grids from 2^28 su; forced here) instead of id order: every tie-break is on the id
+    (engine.cpp:375-378), so nothing may change.  120 ticks cross two re-ordering passes and two rebuilds;
+    multi-cell pedestrians make sure only centres are listed."""
+    monkeypatch.setenv("SFC_PED_ORDER", "1")
+    text = sc.DESK64 if name == "desk64" else sc.EXTRA.get(name) or dict(sc.acceptance3_scenarios())[name]
+    gpu = shim.Sim.from_scenario(product_lib, text)
+    cpu = oracle.OracleSim.from_scenario(text)
+    for step in range(4):
+        np.testing.assert_array_equal(gpu.run(30), cpu.run(30), err_msg=f"{name} moved")
+        assert_state_equal(gpu, cpu, f"{name} position order tick {30 * (step + 1)}")
+
+
 @pytest.mark.parametrize("path", ["window", "scatter-list", "listwalk-list", "pairs-list"])
 def test_tile_stamps_survive_the_epoch_period(product_lib, monkeypatch, path):
     """The active-tile stamps carry the tick modulo 65535; the engine erases them once per period so
