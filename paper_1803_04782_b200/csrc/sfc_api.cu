@@ -103,6 +103,8 @@ struct sfc_engine {
     int negative_zero = 0;    // the uploaded images held a -0.0f (Ctl::negative_zero): runs end with the normalising pass
     double move_rate = 1.0;   // mean over the population of 1 / walk_period (upload)
     double events_per_window = 0.0; // movement events a field window sees per tick: estimated at upload, measured after every run
+    long long last_rebuild_tick = -1; // ticks done at the last rebuild whose result the tile stamps have tracked since (-1: none)
+    int rebuild_skip = 1;     // SFC_REBUILD_SKIP=0: every rebuild re-rasterizes every tile
     int order_pref = -1;      // per-pedestrian kernels visit the pedestrians in position order: SFC_PED_ORDER=1 / 0, -1: by grid size
     int* order_counts = nullptr; // ordering pass scratch
     long long order_tick = 0; // tick of the last ordering pass
@@ -491,14 +493,24 @@ int enqueue_tick_kernels(sfc_engine* e) {
     return SFC_OK;
 }
 
-int enqueue_rebuild(sfc_engine* e) { // maybe_rebuild body, engine.cpp:540-549
+int enqueue_rebuild(sfc_engine* e, long long now) { // maybe_rebuild body, engine.cpp:540-549; now = ticks done so far
     // (the commit pass only rewrites tiles where the check pass saw a fresh value differ from the image: in a sparse
     // crowd most tiles are all zero before and after)
     unsigned* const changed = e->slab.band ? nullptr : e->rebuild_changed;
-    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 1, 0.0, changed));
+    // With the tile stamps on since the previous rebuild (and not erased in between), the check pass leaves tiles alone
+    // that no mover has reached since: config 4 re-rasterizes a quarter less of its 1.07e9 su.
+    RebuildSkip skip{};
+    const long long last = e->last_rebuild_tick, period = (long long)kEpochPeriod;
+    if (e->rebuild_skip && e->marks.epoch != nullptr && last >= 0 && last < now && last / period == (now - 1) / period) {
+        skip.marks = e->marks;
+        skip.stamp_lo = (unsigned)(last % period) + 1u;
+        skip.stamp_hi = (unsigned)((now - 1) % period) + 1u;
+    }
+    SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 1, 0.0, changed, &skip));
     SFC_CUDA(launch_drift_verdict(e->stream, e->ctl, e->cfg.rebuild_tolerance));
     SFC_CUDA(launch_rebuild(e->stream, e->g, e->tabs, e->peds, e->occ, e->dyn, nullptr, e->ctl, 2, 0.0, changed));
     e->counters.kernel_launches += 3;
+    e->last_rebuild_tick = changed != nullptr ? now : -1;
     return SFC_OK;
 }
 
@@ -606,6 +618,7 @@ int select_k5_path(sfc_engine* e, long long P, bool allow_list) {
         const int lazy = field && (e->field_lazy_pref >= 0 ? e->field_lazy_pref : events_per_window < 24.0);
         if (use != (e->marks.epoch != nullptr) || window != e->k5_window || walk_only != e->k5_listwalk_only || pairs != e->k5_pairs ||
             field != e->k5_field || lazy != e->field_lazy) {
+            if (use != (e->marks.epoch != nullptr)) e->last_rebuild_tick = -1; // (the stamps no longer cover the span since the last rebuild)
             e->marks = use ? m : TileMarks{};
             e->k5_window = window;
             e->k5_listwalk_only = walk_only;
@@ -660,6 +673,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_GRAPH_TICKS")) e->graph_ticks = std::clamp(std::atoi(knob), 1, 64);
+    if (const char* knob = std::getenv("SFC_REBUILD_SKIP")) e->rebuild_skip = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_PED_ORDER")) e->order_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;
     if (const char* knob = std::getenv("SFC_K5_PATH")) {
@@ -993,6 +1007,7 @@ int sfc_upload(sfc_engine* e, const sfc_state_view* v) {
     }
     e->tick = v->tick;
     e->uploaded = true;
+    e->last_rebuild_tick = -1;
     if (!v->dyn_images[0] || !v->dyn_images[1] || !v->dyn_images[2]) { // rasterize_dynamic, scenario.cpp:427
         if (v->dyn_images[0] || v->dyn_images[1] || v->dyn_images[2])
             return fail(e, SFC_E_STATE, "upload: give all three dynamic images or none");
@@ -1103,7 +1118,7 @@ int sfc_run(sfc_engine* e, int64_t ticks, sfc_tick_metrics* metrics, int with_ph
         e->counters.kernel_launches += done * (3 + e->k5_launches);
         t += done;
         if (interval > 0 && (base + t) % interval == 0) {
-            rc = enqueue_rebuild(e);
+            rc = enqueue_rebuild(e, base + t);
             if (rc != SFC_OK) return rc;
         }
         if (base + t - e->order_tick >= kOrderPeriod) {
@@ -1206,7 +1221,7 @@ int sfc_phase(sfc_engine* e, int phase, int64_t* moved) {
             e->counters.kernel_launches += 1;
             const long long interval = e->cfg.rebuild_interval;
             if (interval > 0 && (e->tick + 1) % interval == 0) {
-                rc = enqueue_rebuild(e);
+                rc = enqueue_rebuild(e, e->tick + 1);
                 if (rc != SFC_OK) return rc;
             }
             break;
@@ -1369,7 +1384,7 @@ int sfc_slab_step(sfc_engine* e, int step) {
             e->counters.kernel_launches += 2 + e->k5_launches;
             const long long interval = e->cfg.rebuild_interval;
             if (interval > 0 && (e->tick + 1) % interval == 0) {
-                const int rc = enqueue_rebuild(e);
+                const int rc = enqueue_rebuild(e, e->tick + 1);
                 if (rc != SFC_OK) return rc;
             }
             e->tick += 1; // host shadow; the device counter advanced inside k-5

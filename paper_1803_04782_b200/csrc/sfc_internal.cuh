@@ -353,8 +353,15 @@ long long k5_tile_count(const GridDev& g);
 // rebuild / rasterize_dynamic.  mode 0: write fresh images to `out` (record layout), no compare;
 // mode 1: compare with dyn and record the per-kind drift maxima in ctl; mode 2: overwrite dyn
 // unless ctl holds an error.
+// Rebuild check pass: tiles whose TileMarks stamp lies outside [stamp_lo, stamp_hi] — the ticks since the previous
+// rebuild — are skipped (stamp_lo 0: no skipping).  The caller guarantees the stamps cover that whole span.
+struct RebuildSkip {
+    TileMarks marks;
+    unsigned stamp_lo, stamp_hi;
+};
 cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
-                           float* dyn, float* out, Ctl* ctl, int mode, double tolerance, unsigned* changed = nullptr);
+                           float* dyn, float* out, Ctl* ctl, int mode, double tolerance, unsigned* changed = nullptr,
+                           const RebuildSkip* skip = nullptr);
 // `changed`: one bit per rebuild tile (rebuild_tile_count(g) bits).  Mode 1 sets the bit of every tile where a fresh value
 // differs from the image bit for bit; mode 2 then skips the tiles whose bit is clear and clears the others' (nullptr: every tile).
 long long rebuild_tile_count(const GridDev& g);

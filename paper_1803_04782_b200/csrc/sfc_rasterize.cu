@@ -37,6 +37,7 @@ struct RbArgs {
     int mode;
     int cap; // power of two
     unsigned* changed; // one bit per tile, or nullptr (see launch_rebuild)
+    RebuildSkip skip;  // check pass: tiles no mover has reached since the previous rebuild are left alone
 };
 
 __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
@@ -55,6 +56,17 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     }
 
     const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
+    if (a.mode == 1 && a.skip.stamp_lo != 0u) {
+        // k-4 stamps every tile within field reach of a mover with the tick (TileMarks).  A tile not stamped since the
+        // previous rebuild has seen no k-5 write, and every pedestrian whose field reaches it stands where it stood then:
+        // its images are the fresh ones of that rebuild, bit for bit — nothing to compare, nothing to commit (its
+        // "changed" bit stays clear).  Slab edge tiles also depend on pedestrians only the halo rows show: never skipped.
+        const int mty = tile_y * kRbTileH / kMarkTileH;
+        if (mty >= a.skip.marks.edge_lo && mty < a.skip.marks.edge_hi) {
+            const unsigned stamp = a.skip.marks.epoch[mty * a.skip.marks.tiles_x + tile_x] >> 16;
+            if (stamp < a.skip.stamp_lo || stamp > a.skip.stamp_hi) return; // (uniform)
+        }
+    }
     const int x0 = tile_x * kTileW, y0 = g.row0 + tile_y * kRbTileH;
     const int nx = min(kTileW, g.W - x0), ny = min(kRbTileH, g.row0 + g.rows - y0);
     const int HW = a.t.max_hw, HH = a.t.max_hh;
@@ -312,7 +324,7 @@ cudaError_t prepare_rebuild(const TablesDev& t) {
 long long rebuild_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + kRbTileH - 1) / kRbTileH); }
 
 cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t, const PedArrays& p, const int* occ,
-                           float* dyn, float* out, Ctl* ctl, int mode, double /*tolerance*/, unsigned* changed) {
+                           float* dyn, float* out, Ctl* ctl, int mode, double /*tolerance*/, unsigned* changed, const RebuildSkip* skip) {
     RbArgs a;
     a.g = g;
     a.t = t;
@@ -323,6 +335,7 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     a.ctl = ctl;
     a.mode = mode;
     a.changed = changed;
+    a.skip = (skip != nullptr && mode == 1 && changed != nullptr && skip->marks.epoch != nullptr) ? *skip : RebuildSkip{};
     a.tiles_x = (g.W + kTileW - 1) / kTileW;
     a.cap = rebuild_cap(t);
     if (const char* knob = std::getenv("SFC_REBUILD_CAP")) // (tests: a short sorted list forces the id-range rounds)
