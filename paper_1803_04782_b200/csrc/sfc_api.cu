@@ -673,6 +673,7 @@ int sfc_create(const sfc_config* cfg, const sfc_tables* tables, sfc_engine** out
     e->cfg = *cfg;
     e->device = cfg->device;
     if (const char* knob = std::getenv("SFC_GRAPH_TICKS")) e->graph_ticks = std::clamp(std::atoi(knob), 1, 64);
+    chain_configure();
     if (const char* knob = std::getenv("SFC_REBUILD_SKIP")) e->rebuild_skip = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_PED_ORDER")) e->order_pref = std::atoi(knob) != 0;
     if (const char* knob = std::getenv("SFC_K5_TILE_ROWS")) e->k5_tile_rows = std::atoi(knob) == 4 ? 4 : 8;

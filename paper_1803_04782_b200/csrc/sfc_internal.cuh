@@ -90,7 +90,8 @@ __device__ __forceinline__ void chain_release(bool on) {
 }
 __device__ __forceinline__ void chain_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-bool chain_enabled(); // sfc_ped_kernels.cu
+bool chain_enabled();   // sfc_ped_kernels.cu
+void chain_configure(); // reads SFC_CHAIN (sfc_create)
 
 template <typename... Params, typename... Args>
 cudaError_t launch_chained(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {

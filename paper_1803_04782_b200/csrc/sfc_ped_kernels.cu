@@ -10,6 +10,7 @@
 // the occupancy grid plus the per-pedestrian decision arrays: same result, no per-su
 // temporaries, no atomics, no full-grid clear (the reference's k-1).
 
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 
@@ -760,12 +761,19 @@ cudaError_t launch_tick_advance(cudaStream_t s, Ctl* ctl) {
     return cudaGetLastError();
 }
 
+namespace {
+std::atomic<int> g_chain{-1}; // -1: not read yet
+}
+
+// (read again whenever an engine is created, so a process can switch between engines — tests do)
+void chain_configure() {
+    const char* knob = std::getenv("SFC_CHAIN");
+    g_chain.store(knob == nullptr || std::atoi(knob) != 0 ? 1 : 0, std::memory_order_relaxed);
+}
+
 bool chain_enabled() {
-    static const bool on = [] {
-        const char* knob = std::getenv("SFC_CHAIN");
-        return knob == nullptr || std::atoi(knob) != 0;
-    }();
-    return on;
+    if (g_chain.load(std::memory_order_relaxed) < 0) chain_configure();
+    return g_chain.load(std::memory_order_relaxed) != 0;
 }
 
 long long order_chunks(long long cells) { return (cells + kOrdChunk - 1) / kOrdChunk; }

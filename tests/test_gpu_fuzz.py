@@ -1,7 +1,8 @@
 """Seeded random scenarios against the oracle: grid extents (ragged, tiny, not a multiple of the 16-byte
 staging group), field and pedestrian geometries, densities, chunk widths, boundaries, walk periods,
 regulation, rebuild intervals — each through the engine's own choice of k-5 kernel and through a randomly
-forced one (pair / field / list-walk / window / scatter kernel, row slabs, band-swapped pass).  Bit-exact."""
+forced one (pair / field / list-walk / window / scatter kernel, row slabs, band-swapped pass), some with the
+pedestrian kernels in position order, plain launches, or the tile stamps on.  Bit-exact."""
 import os
 import random
 
@@ -60,6 +61,13 @@ def test_random_scenarios_match_the_oracle(product_lib, monkeypatch, case):
     rng = random.Random(SEED + case)
     text, dims = random_scenario(rng)
     knobs = forced(rng, dims) if case % 2 else {}
+    extras = random.Random(SEED + case + 10 ** 6)  # (a separate stream: the cases above keep their scenarios)
+    if extras.random() < 0.3:
+        knobs["SFC_PED_ORDER"] = "1"  # k-2 ... k-4 in position order
+    if extras.random() < 0.2:
+        knobs["SFC_CHAIN"] = "0"  # plain launches
+    if extras.random() < 0.3 and knobs.get("SFC_K5_PATH") in (None, "pairs", "listwalk") and "SFC_SLABS" not in knobs and "SFC_BANDS" not in knobs:
+        knobs["SFC_K5_ACTIVE_LIST"] = "1"  # tile stamps on: rebuilds may skip untouched tiles
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     try:
