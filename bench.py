@@ -543,7 +543,7 @@ def main():
         run_e2e = lambda: (engine.step_resident(TICKS_PER_STEP), engine.download_centers())  # noqa: E731
     else:
         engine.download(state)
-        e2e_call = f"socfield.Engine.run(state, {TICKS_PER_STEP}) on host SimState (pageable std::vector storage)"
+        e2e_call = f"socfield.Engine.run(state, {TICKS_PER_STEP}) on host SimState (its std::vector storage page-locked by the engine: include/socfield/pinned.hpp)"
         run_e2e = lambda: engine.run(state, TICKS_PER_STEP)  # noqa: E731
     for _ in range(2):
         run_e2e()
