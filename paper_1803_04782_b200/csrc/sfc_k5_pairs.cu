@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArg
     unsigned long long* const sT = reinterpret_cast<unsigned long long*>(smem_raw);
     PairEntry* const sE = reinterpret_cast<PairEntry*>(sT + t_entries);
     WarpScratch* const ws = reinterpret_cast<WarpScratch*>(sE + kSects * kGroupBits) + warp;
+    uint32_t* const sSel = reinterpret_cast<uint32_t*>(reinterpret_cast<WarpScratch*>(sE + kSects * kGroupBits) + kWarps); // selector of every event byte
+    for (int i = tid; i < 256; i += kThreads) sSel[i] = selector((uint32_t)i);
     for (int i = tid; i < t_entries; i += kThreads) sT[i] = a.T[i];
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.E);
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, RED ? 4 : 2) k5_pairs_kernel(PairArg
         for (int p = 0; p < PASSES; ++p) {
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, code[p] != 0u);
             if (bal != 0u) { // (warp-uniform)
-                if (code[p]) ws->sel[(2 * p + r0) * kPitch + c] = make_uint2(selector(code[p] & 0xFFu), selector(code[p] >> 8));
+                if (code[p]) ws->sel[(2 * p + r0) * kPitch + c] = make_uint2(sSel[code[p] & 0xFFu], sSel[code[p] >> 8]);
                 if (bal & 0xFFFFu) rows_nz |= 1u << (2 * p);
                 if (bal >> 16) rows_nz |= 2u << (2 * p);
             }
@@ -392,7 +394,7 @@ bool build_host_tables(const WalkListsHost& w, int chunk_k, PairTablesHost* out)
 
 size_t pairs_smem(const PairTables& t) {
     return (((size_t)t.fh << t.fw) * sizeof(unsigned long long) + sizeof(PairEntry) * kSects * kGroupBits +
-            sizeof(WarpScratch) * kWarps + 15) & ~(size_t)15;
+            sizeof(WarpScratch) * kWarps + 256 * sizeof(uint32_t) + 15) & ~(size_t)15;
 }
 
 } // namespace
