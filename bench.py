@@ -587,8 +587,10 @@ def main():
         "gpu_launches": launches,
         "phase_us_per_tick": {"k1": phase_us[0], "k2": phase_us[1], "k3": phase_us[2], "k4": phase_us[3], "k5": phase_us[4]},
         "tick_us": tick_us,
+        # (whole tick on SURVEY's 200 B per su + 200 B per pedestrian; on a sparse crowd that algorithmic figure exceeds
+        # the peak and says nothing — no fraction is printed for it, `frac` above is on the bytes actually moved)
         "roofline": dict(k5_roofline(args.workload, C, k5_us, K5_KERNEL.get(c1.get("k5_path"), "k-5")),
-                         whole_tick_gbs=tick_gbs, whole_tick_frac=tick_gbs / peak),
+                         whole_tick_gbs=tick_gbs, whole_tick_frac=(tick_gbs / peak) if tick_gbs <= peak else None),
         "cpu_baseline": cpu,
     }
     if not args.no_configs and world == 1:
