@@ -50,12 +50,13 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     const GridDev g = a.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (a.mode == 2 && a.ctl->error_code != 0) return;
+    const int tile_x = blockIdx.x, tile_y = blockIdx.y; // (a 2-D grid: no division)
+    const unsigned tile = (unsigned)tile_y * (unsigned)a.tiles_x + (unsigned)tile_x;
     if (a.mode == 2 && a.changed != nullptr) { // the check pass found this tile's images equal to the fresh ones, bit for bit
-        const unsigned word = a.changed[blockIdx.x >> 5], bit = 1u << (blockIdx.x & 31);
+        const unsigned word = a.changed[tile >> 5], bit = 1u << (tile & 31);
         if (!(word & bit)) return; // (uniform)
     }
 
-    const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
     if (a.mode == 1 && a.skip.stamp_lo != 0u) {
         // k-4 stamps every tile within field reach of a mover with the tick (TileMarks).  A tile not stamped since the
         // previous rebuild has seen no k-5 write, and every pedestrian whose field reaches it stands where it stood then:
@@ -97,40 +98,56 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         // collect the pedestrian centres of the region (any order; sorted below); (row, column) of a thread's cells
         // advance incrementally — no division, one wrap per axis
         const bool narrow = RW <= g.W; // (a field wider than the grid wraps more than once: the general path)
+        auto consider = [&](long long idx, int wx, int wy, int ryi, int rxi) {
+            const int id = a.occ[idx];
+            if (id < id_lo || id >= id_hi) return; // (empty su hold -1)
+            const int2 c = a.p.center[id];
+            if (c.x != wx || c.y != wy) return; // a footprint su, not the centre
+            const int pos = atomicAdd(&s_count, 1);
+            if (pos < a.cap) {
+                const uint32_t attr = a.p.attr[id];
+                keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
+                            ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+            }
+        };
         {
             const int dr = kRbThreads / RW, dc = kRbThreads - dr * RW;
             int ryi = tid / RW, rxi = tid - ryi * RW;
-            for (; ryi < RH; rxi += dc, ryi += dr) {
-                if (rxi >= RW) {
-                    rxi -= RW;
-                    if (++ryi >= RH) break;
-                }
-                int wx = xs + rxi, wy = ys + ryi;
-                long long idx;
-                if (narrow) {
-                    const long long row = cell_index(g, 0, wy); // -1: the row does not exist / is not resident
-                    if (row < 0) continue;
-                    if (g.closed) {
-                        if (wx < 0 || wx >= g.W) continue;
-                    } else {
-                        wx += wx < 0 ? g.W : (wx >= g.W ? -g.W : 0);
+            const int ly0 = ys - g.row0 + g.halo; // local row of the region's first row, if it is resident unwrapped
+            if (narrow && xs >= 0 && xs + RW <= g.W && ys >= 0 && ys + RH <= g.H && ly0 >= 0 && ly0 + RH <= g.rows + 2 * g.halo) {
+                // the region lies inside the grid and inside the resident rows (nearly every tile): plain indexing
+                const long long base = (long long)ly0 * g.W + xs;
+                for (; ryi < RH; rxi += dc, ryi += dr) {
+                    if (rxi >= RW) {
+                        rxi -= RW;
+                        if (++ryi >= RH) break;
                     }
-                    idx = row + wx;
-                } else {
-                    idx = cell_index(g, wx, wy);
-                    if (idx < 0) continue;
-                    if (!g.closed) wx = emod(wx, g.W);
+                    consider(base + (long long)ryi * g.W + rxi, xs + rxi, ys + ryi, ryi, rxi);
                 }
-                if (!g.closed) wy = emod(wy, g.H);
-                const int id = a.occ[idx];
-                if (id < id_lo || id >= id_hi) continue; // (empty su hold -1)
-                const int2 c = a.p.center[id];
-                if (c.x != wx || c.y != wy) continue; // a footprint su, not the centre
-                const int pos = atomicAdd(&s_count, 1);
-                if (pos < a.cap) {
-                    const uint32_t attr = a.p.attr[id];
-                    keys[pos] = ((unsigned long long)(uint32_t)id << 32) | ((unsigned long long)(8191 - ryi) << 19) |
-                                ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
+            } else {
+                for (; ryi < RH; rxi += dc, ryi += dr) {
+                    if (rxi >= RW) {
+                        rxi -= RW;
+                        if (++ryi >= RH) break;
+                    }
+                    int wx = xs + rxi, wy = ys + ryi;
+                    long long idx;
+                    if (narrow) {
+                        const long long row = cell_index(g, 0, wy); // -1: the row does not exist / is not resident
+                        if (row < 0) continue;
+                        if (g.closed) {
+                            if (wx < 0 || wx >= g.W) continue;
+                        } else {
+                            wx += wx < 0 ? g.W : (wx >= g.W ? -g.W : 0);
+                        }
+                        idx = row + wx;
+                    } else {
+                        idx = cell_index(g, wx, wy);
+                        if (idx < 0) continue;
+                        if (!g.closed) wx = emod(wx, g.W);
+                    }
+                    if (!g.closed) wy = emod(wy, g.H);
+                    consider(idx, wx, wy, ryi, rxi);
                 }
             }
         }
@@ -232,10 +249,10 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     }
     if (a.changed != nullptr) { // the tile's "commit needed" bit: set by the check pass, consumed by the commit pass
         if (a.mode == 1) {
-            if (__any_sync(0xFFFFFFFFu, differs) && lane == 0) atomicOr(&a.changed[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
+            if (__any_sync(0xFFFFFFFFu, differs) && lane == 0) atomicOr(&a.changed[tile >> 5], 1u << (tile & 31));
         } else if (a.mode == 2) {
             __syncthreads(); // (every thread of the CTA has read the word)
-            if (tid == 0) atomicAnd(&a.changed[blockIdx.x >> 5], ~(1u << (blockIdx.x & 31)));
+            if (tid == 0) atomicAnd(&a.changed[tile >> 5], ~(1u << (tile & 31)));
         }
     }
     if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
@@ -341,8 +358,9 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     if (const char* knob = std::getenv("SFC_REBUILD_CAP")) // (tests: a short sorted list forces the id-range rounds)
         a.cap = std::min(a.cap, next_pow2(std::max(1, std::atoi(knob))));
     const size_t smem = rebuild_smem(t);
-    const long long blocks = (long long)a.tiles_x * ((g.rows + kRbTileH - 1) / kRbTileH);
-    rebuild_kernel<<<(unsigned)blocks, kRbThreads, smem, s>>>(a);
+    const int tiles_y = (g.rows + kRbTileH - 1) / kRbTileH;
+    if (tiles_y > 65535) return cudaErrorInvalidConfiguration; // (262 140 rows per slab / band)
+    rebuild_kernel<<<dim3((unsigned)a.tiles_x, (unsigned)tiles_y), kRbThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
