@@ -40,6 +40,9 @@ struct RbArgs {
     RebuildSkip skip;  // check pass: tiles no mover has reached since the previous rebuild are left alone
 };
 
+// MODE 0: rasterize into `out`; 1: check pass (compare, drift, "changed" bits); 2: commit pass (replace the images).
+// (A compile-time mode: the commit pass does not carry the check pass's prefetched records in registers.)
+template <int MODE>
 __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw); // [cap]
@@ -49,15 +52,15 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
 
     const GridDev g = a.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.mode == 2 && a.ctl->error_code != 0) return;
+    if (MODE == 2 && a.ctl->error_code != 0) return;
     const int tile_x = blockIdx.x, tile_y = blockIdx.y; // (a 2-D grid: no division)
     const unsigned tile = (unsigned)tile_y * (unsigned)a.tiles_x + (unsigned)tile_x;
-    if (a.mode == 2 && a.changed != nullptr) { // the check pass found this tile's images equal to the fresh ones, bit for bit
+    if (MODE == 2 && a.changed != nullptr) { // the check pass found this tile's images equal to the fresh ones, bit for bit
         const unsigned word = a.changed[tile >> 5], bit = 1u << (tile & 31);
         if (!(word & bit)) return; // (uniform)
     }
 
-    if (a.mode == 1 && a.skip.stamp_lo != 0u) {
+    if (MODE == 1 && a.skip.stamp_lo != 0u) {
         // k-4 stamps every tile within field reach of a mover with the tick (TileMarks).  A tile not stamped since the
         // previous rebuild has seen no k-5 write, and every pedestrian whose field reaches it stands where it stood then:
         // its images are the fresh ones of that rebuild, bit for bit — nothing to compare, nothing to commit (its
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     float4 old[6];
 #pragma unroll
     for (int v = 0; v < 6; ++v)
-        old[v] = (active && a.mode == 1) ? reinterpret_cast<const float4*>(a.dyn + my_cell * 24)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        old[v] = (active && MODE == 1) ? reinterpret_cast<const float4*>(a.dyn + my_cell * 24)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
 
     // The centres of the region are taken in ROUNDS of ascending id ranges: one round over every id when
     // they fit the sorted list (the usual case), else as many equal id ranges as bring a range's expected
@@ -217,16 +220,16 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
     float drift[kKinds] = {0.0f, 0.0f, 0.0f};
     bool differs = false;
     if (active) { // the su's 96-byte record as six 16-byte accesses
-        float4* const rec = reinterpret_cast<float4*>((a.mode == 0 ? a.out : a.dyn) + my_cell * 24);
+        float4* const rec = reinterpret_cast<float4*>((MODE == 0 ? a.out : a.dyn) + my_cell * 24);
         bool blank = false; // nothing in reach and the record is all +0.0f: equal, no drift
-        if (a.mode == 1 && !have_acc) {
+        if (MODE == 1 && !have_acc) {
             uint32_t any_bits = 0u;
 #pragma unroll
             for (int v = 0; v < 6; ++v)
                 any_bits |= __float_as_uint(old[v].x) | __float_as_uint(old[v].y) | __float_as_uint(old[v].z) | __float_as_uint(old[v].w);
             blank = any_bits == 0u;
         }
-        if (a.mode == 1 && !blank) {
+        if (MODE == 1 && !blank) {
 #pragma unroll
             for (int v = 0; v < 6; ++v) {
                 const float o[4] = {old[v].x, old[v].y, old[v].z, old[v].w};
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
                     differs = differs || __float_as_uint(o[c]) != __float_as_uint(fresh);
                 }
             }
-        } else if (a.mode != 1) {
+        } else if (MODE != 1) {
 #pragma unroll
             for (int v = 0; v < 6; ++v)
                 rec[v] = have_acc ? make_float4(acc[(4 * v) * kRbThreads + tid], acc[(4 * v + 1) * kRbThreads + tid],
@@ -248,14 +251,14 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         }
     }
     if (a.changed != nullptr) { // the tile's "commit needed" bit: set by the check pass, consumed by the commit pass
-        if (a.mode == 1) {
+        if (MODE == 1) {
             if (__any_sync(0xFFFFFFFFu, differs) && lane == 0) atomicOr(&a.changed[tile >> 5], 1u << (tile & 31));
-        } else if (a.mode == 2) {
+        } else if (MODE == 2) {
             __syncthreads(); // (every thread of the CTA has read the word)
             if (tid == 0) atomicAnd(&a.changed[tile >> 5], ~(1u << (tile & 31)));
         }
     }
-    if (a.mode == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
+    if (MODE == 1) { // max_abs_difference (fields.cpp:144-150) reduced warp -> CTA -> grid
         const bool some = __any_sync(0xFFFFFFFFu, drift[0] > 0.0f || drift[1] > 0.0f || drift[2] > 0.0f);
 #pragma unroll
         for (int k = 0; k < kKinds; ++k) {
@@ -334,8 +337,17 @@ size_t rebuild_smem(const TablesDev& t) {
 
 // Raises the dynamic shared-memory limit ahead of time (must not happen inside a graph capture).
 cudaError_t prepare_rebuild(const TablesDev& t) {
-    static SmemGrant grant;
-    return grant.raise(reinterpret_cast<const void*>(rebuild_kernel), rebuild_smem(t), 48 * 1024);
+    static SmemGrant grant[3];
+    cudaError_t e = grant[0].raise(reinterpret_cast<const void*>(rebuild_kernel<0>), rebuild_smem(t), 48 * 1024);
+    if (e == cudaSuccess) e = grant[1].raise(reinterpret_cast<const void*>(rebuild_kernel<1>), rebuild_smem(t), 48 * 1024);
+    if (e == cudaSuccess) e = grant[2].raise(reinterpret_cast<const void*>(rebuild_kernel<2>), rebuild_smem(t), 48 * 1024);
+    // the passes are latency-bound on small CTAs: ask for the largest shared-memory carve-out so that shared memory
+    // does not cap the resident CTAs below what the registers allow (a hint; failure is harmless)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(rebuild_kernel<0>), cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(rebuild_kernel<1>), cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(rebuild_kernel<2>), cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    (void)cudaGetLastError();
+    return e;
 }
 
 long long rebuild_tile_count(const GridDev& g) { return (long long)((g.W + kTileW - 1) / kTileW) * ((g.rows + kRbTileH - 1) / kRbTileH); }
@@ -360,7 +372,10 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     const size_t smem = rebuild_smem(t);
     const int tiles_y = (g.rows + kRbTileH - 1) / kRbTileH;
     if (tiles_y > 65535) return cudaErrorInvalidConfiguration; // (262 140 rows per slab / band)
-    rebuild_kernel<<<dim3((unsigned)a.tiles_x, (unsigned)tiles_y), kRbThreads, smem, s>>>(a);
+    const dim3 grid((unsigned)a.tiles_x, (unsigned)tiles_y);
+    if (mode == 0) rebuild_kernel<0><<<grid, kRbThreads, smem, s>>>(a);
+    else if (mode == 1) rebuild_kernel<1><<<grid, kRbThreads, smem, s>>>(a);
+    else rebuild_kernel<2><<<grid, kRbThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
