@@ -38,6 +38,8 @@ struct RbArgs {
     int cap; // power of two
     unsigned* changed; // one bit per tile, or nullptr (see launch_rebuild)
     RebuildSkip skip;  // check pass: tiles no mover has reached since the previous rebuild are left alone
+    int rw_full, dr_full, dc_full; // region width of a full-width tile and the scan's (row, column) step for it
+    unsigned inv_rw_full;          // tid / rw_full = umulhi(tid, inv_rw_full) for tid < 2^16
 };
 
 // MODE 0: rasterize into `out`; 1: check pass (compare, drift, "changed" bits); 2: commit pass (replace the images).
@@ -114,8 +116,10 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
             }
         };
         {
-            const int dr = kRbThreads / RW, dc = kRbThreads - dr * RW;
-            int ryi = tid / RW, rxi = tid - ryi * RW;
+            // (the divisions by the region width are done on the host for full-width tiles)
+            const bool full = RW == a.rw_full;
+            const int dr = full ? a.dr_full : kRbThreads / RW, dc = full ? a.dc_full : kRbThreads - dr * RW;
+            int ryi = full ? (int)__umulhi((unsigned)tid, a.inv_rw_full) : tid / RW, rxi = tid - ryi * RW;
             const int ly0 = ys - g.row0 + g.halo; // local row of the region's first row, if it is resident unwrapped
             if (narrow && xs >= 0 && xs + RW <= g.W && ys >= 0 && ys + RH <= g.H && ly0 >= 0 && ly0 + RH <= g.rows + 2 * g.halo) {
                 // the region lies inside the grid and inside the resident rows (nearly every tile): plain indexing
@@ -366,6 +370,10 @@ cudaError_t launch_rebuild(cudaStream_t s, const GridDev& g, const TablesDev& t,
     a.changed = changed;
     a.skip = (skip != nullptr && mode == 1 && changed != nullptr && skip->marks.epoch != nullptr) ? *skip : RebuildSkip{};
     a.tiles_x = (g.W + kTileW - 1) / kTileW;
+    a.rw_full = kTileW + 2 * t.max_hw;
+    a.dr_full = kRbThreads / a.rw_full;
+    a.dc_full = kRbThreads - a.dr_full * a.rw_full;
+    a.inv_rw_full = 0xFFFFFFFFu / (unsigned)a.rw_full + 1u;
     a.cap = rebuild_cap(t);
     if (const char* knob = std::getenv("SFC_REBUILD_CAP")) // (tests: a short sorted list forces the id-range rounds)
         a.cap = std::min(a.cap, next_pow2(std::max(1, std::atoi(knob))));
