@@ -103,8 +103,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
         // collect the pedestrian centres of the region (any order; sorted below); (row, column) of a thread's cells
         // advance incrementally — no division, one wrap per axis
         const bool narrow = RW <= g.W; // (a field wider than the grid wraps more than once: the general path)
-        auto consider = [&](long long idx, int wx, int wy, int ryi, int rxi) {
-            const int id = a.occ[idx];
+        auto consider_id = [&](int id, int wx, int wy, int ryi, int rxi) {
             if (id < id_lo || id >= id_hi) return; // (empty su hold -1)
             const int2 c = a.p.center[id];
             if (c.x != wx || c.y != wy) return; // a footprint su, not the centre
@@ -115,6 +114,7 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
                             ((unsigned long long)(8191 - rxi) << 6) | (unsigned long long)((attr >> 3) & 0x3Fu);
             }
         };
+        auto consider = [&](long long idx, int wx, int wy, int ryi, int rxi) { consider_id(a.occ[idx], wx, wy, ryi, rxi); };
         {
             // (the divisions by the region width are done on the host for full-width tiles)
             const bool full = RW == a.rw_full;
@@ -123,13 +123,31 @@ __global__ void __launch_bounds__(kRbThreads) rebuild_kernel(RbArgs a) {
             const int ly0 = ys - g.row0 + g.halo; // local row of the region's first row, if it is resident unwrapped
             if (narrow && xs >= 0 && xs + RW <= g.W && ys >= 0 && ys + RH <= g.H && ly0 >= 0 && ly0 + RH <= g.rows + 2 * g.halo) {
                 // the region lies inside the grid and inside the resident rows (nearly every tile): plain indexing
+                // (four cells per trip: the occupancy loads of a trip are in flight together — a 7 x 7 field's region is
+                // three cells per thread, one round trip instead of three)
                 const long long base = (long long)ly0 * g.W + xs;
-                for (; ryi < RH; rxi += dc, ryi += dr) {
-                    if (rxi >= RW) {
-                        rxi -= RW;
-                        if (++ryi >= RH) break;
+                while (ryi < RH) {
+                    int id[4], by[4], bx[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        id[q] = kNoPed;
+                        by[q] = bx[q] = 0;
+                        if (ryi < RH) {
+                            if (rxi >= RW) {
+                                rxi -= RW;
+                                ++ryi;
+                            }
+                            if (ryi < RH) {
+                                id[q] = a.occ[base + (long long)ryi * g.W + rxi];
+                                by[q] = ryi;
+                                bx[q] = rxi;
+                            }
+                            rxi += dc;
+                            ryi += dr;
+                        }
                     }
-                    consider(base + (long long)ryi * g.W + rxi, xs + rxi, ys + ryi, ryi, rxi);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) consider_id(id[q], xs + bx[q], ys + by[q], by[q], bx[q]);
                 }
             } else {
                 for (; ryi < RH; rxi += dc, ryi += dr) {
