@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NK == 3 ? 256 : kMaxThreads) k5_field_kernel(F
     constexpr int KH = K / 2;                // partials per (kind, group) and lane: the even or the odd slots
     constexpr int KO = kSects * KH * 32;     // partial doubles per kind and warp
 #ifndef SFC_FIELD_EV
-#define SFC_FIELD_EV (LAZY ? 2 : 4)
+#define SFC_FIELD_EV (LAZY ? 2 : (NK == 3 ? 8 : 4))
 #endif
     constexpr int EV = SFC_FIELD_EV;         // events a lane looks up before it folds any of them
     constexpr int PW = NK * KO;              // ... per warp
