@@ -3,9 +3,12 @@
 # each headline k-5 kernel (summary = per-source-line shares, metrics = the raw page's key counters).
 set -u
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/r2_launches_bench.csv \
+[ "${SKIP_LAUNCHES:-0}" = 1 ] || ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/r2_launches_bench.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-configs > gpurun_out/r2_launches_bench.out 2>&1
-for spec in "c2 k5_pairs r2_k5_pairs_c2" "c4r k5_pairs r2_k5_pairs_c4r" "paper1000 k5_pairs r2_k5_pairs_paper1000" "c3 k5_field r2_k5_field_c3" "c5 k5_field r2_k5_field_c5"; do
+DEFAULT_SPECS=("c2 k5_pairs r2_k5_pairs_c2" "c4r k5_pairs r2_k5_pairs_c4r" "paper1000 k5_pairs r2_k5_pairs_paper1000" "c3 k5_field r2_k5_field_c3" "c5 k5_field r2_k5_field_c5")
+# FIELD_ONLY=1 re-captures just the large-field kernel (after a change that touched only sfc_k5_writeback.cu)
+[ "${FIELD_ONLY:-0}" = 1 ] && DEFAULT_SPECS=("c3 k5_field r2_k5_field_c3" "c5 k5_field r2_k5_field_c5")
+for spec in "${DEFAULT_SPECS[@]}"; do
   set -- $spec
   bash profiles/profile_k5.sh $1 $2 $3
   python - "$3" <<'PY'
