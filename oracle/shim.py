@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE.  One Python class, `Sim`, drives any build of the shim:
 
 * ``load_ref()``      -> oracle/_ref/libsocfield_ref.so      (unmodified reference, CPU)
-* ``load_product()``  -> paper_1803_04782_b200/lib/libsocfield_b200_shim.so (CUDA engine)
+* ``load_product()``  -> oracle/build/libsocfield_b200_shim.so (the same shim over the CUDA engine)
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference arm may
 import this module with the reference library; the product never does.
@@ -19,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 REF_LIB = os.path.join(HERE, "_ref", "libsocfield_ref.so")
-PRODUCT_LIB = os.path.join(ROOT, "paper_1803_04782_b200", "lib", "libsocfield_b200_shim.so")
+PRODUCT_LIB = os.path.join(HERE, "build", "libsocfield_b200_shim.so")
 
 ERR_NAMES = {1: "IntegrityError", 2: "ConfigError", 3: "ParseError", 4: "SeedingError", 5: "Error"}
 

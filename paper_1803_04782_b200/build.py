@@ -6,8 +6,10 @@ Produces, under paper_1803_04782_b200/lib/ (git-ignored, shipped to the GPU box 
 
   libsocfield_cuda.so        the sm_100a kernels + C ABI (include/socfield_cuda.h); nvcc
   libsocfield_b200.so        the C++ host mirror of the socfield API (include/socfield/*.hpp); g++
-  libsocfield_b200_shim.so   oracle/socfield_shim.cpp compiled against the mirror (test driver)
   socfield/_core*.so         pybind11 module with the reference's Python surface
+
+and, under oracle/build/ (test infrastructure, not product): libsocfield_b200_shim.so, oracle/socfield_shim.cpp
+compiled against the mirror — the same flat-C driver the tests run the unmodified reference through.
 
 nvcc cross-compiles for sm_100a without a GPU, so this runs in the CPU-only build container.
 """
@@ -97,13 +99,16 @@ def build_host(force: bool = False, verbose: bool = True) -> str:
 
 def build_shim(force: bool = False, verbose: bool = True) -> str:
     host = build_host(force, verbose)
-    target = os.path.join(LIB, "libsocfield_b200_shim.so")
+    outdir = os.path.join(ROOT, "oracle", "build")  # a test driver: kept out of the product's lib/
+    os.makedirs(outdir, exist_ok=True)
+    target = os.path.join(outdir, "libsocfield_b200_shim.so")
     src = os.path.join(ROOT, "oracle", "socfield_shim.cpp")
     hdr = os.path.join(ROOT, "oracle", "socfield_shim.h")
     if force or _newer(target, [src, hdr, host] + _headers()):
         _run([CXX, *CXX_FLAGS, "-Wno-comment", "-I" + INCLUDE, "-I" + os.path.join(ROOT, "oracle"),
               '-DSHIM_IMPL_NAME="b200-cuda"', "-shared", "-o", target, src,
-              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", *STDCXX, "-Wl,-rpath,$ORIGIN"], verbose)
+              "-L" + LIB, "-lsocfield_b200", "-lsocfield_cuda", *STDCXX,
+              "-Wl,-rpath,$ORIGIN/../../paper_1803_04782_b200/lib"], verbose)
     return target
 
 

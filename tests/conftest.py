@@ -52,6 +52,6 @@ def product_lib():
     from oracle import shim
 
     if not shim.have_product():
-        pytest.fail("paper_1803_04782_b200/lib/libsocfield_b200_shim.so missing: run "
+        pytest.fail("oracle/build/libsocfield_b200_shim.so missing: run "
                     "`python -m paper_1803_04782_b200.build` — the product has no CPU fallback")
     return shim.load_product()
